@@ -1,0 +1,286 @@
+"""Benchmark: M elements/s for energy + gradient + Hessian + BSR assembly (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3|c4|c5] [--mode deterministic|atomic|ordered]
+
+One step = one Assembler::assemble() of the whole configuration on device-resident inputs
+(activation refresh, element kernels, SPD projection where the config asks for it, gradient +
+BSR assembly, energy and finiteness reduction). Multi-GPU: one process per GPU, each rank
+assembles its own replica of the configuration ("scaling": "weak"); max-over-ranks device time.
+The `cpu_baseline` / `--impl reference` leg runs the unmodified reference (oracle/_ref/ref_driver,
+reference headers compiled in place, `source` backend, all host threads) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic FP64 flops per element: tape plan ops + (n_qp-1)*outputs for
+# quadrature accumulation + outputs for the global accumulation.
+FLOPS = {"tet4": 4406 + 157, "tet10": 4 * 23164 + 3 * 931 + 931, "membrane": 5622 + 91, "bending": 1009 + 157,
+         "contact": 2811 + 157, "inertia": 23 + 13}
+# compulsory bytes per element: unique inputs once + unique outputs once
+BYTES = {"c1": 223.0, "c2": 211.0, "c3": 2941.0, "c4": 163.0, "c5": 211.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--mode", default="deterministic", choices=["deterministic", "atomic", "ordered"])
+    p.add_argument("--no-spd", action="store_true", help="disable the config's SPD projection")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-n", type=int, default=0, help="reference sample grid size (default per config)")
+    return p.parse_args()
+
+
+def make_case(cfg: str):
+    from paper_2303_02156_b200 import configs as C
+    return {"c1": C.config1, "c2": C.config2, "c3": C.config3, "c4": C.config4, "c5": C.config5}[cfg]()
+
+
+def config_meta(cfg: str):
+    return {
+        "c1": dict(workload="config1: linear-tet Stable NH, 20^3 Kuhn grid, 48,000 tets", spd=False),
+        "c2": dict(workload="config2: linear-tet Stable NH, 100^3 Kuhn grid, 6,000,000 tets, SPD projection", spd=True),
+        "c3": dict(workload="config3: quadratic tet10 Stable NH, 40^3 grid, 384,000 elements, 4-pt rule", spd=False),
+        "c4": dict(workload="config4: cloth 1000x1000, StVK membrane + hinge bending", spd=False),
+        "c5": dict(workload="config5: config2 tets + inertia + 4,000,000 point-triangle barrier pairs, SPD", spd=True),
+    }[cfg]
+
+
+def flops_per_step(cfg: str, case) -> float:
+    if case.kind == "tet4":
+        return FLOPS["tet4"] * case.conn.shape[0]
+    if case.kind == "tet10":
+        return FLOPS["tet10"] * case.conn.shape[0]
+    if case.kind == "cloth":
+        return FLOPS["membrane"] * case.conn.shape[0] + FLOPS["bending"] * case.extra["flaps"].shape[0]
+    return (FLOPS["tet4"] * case.conn.shape[0] + FLOPS["contact"] * case.extra["pairs"].shape[0]
+            + FLOPS["inertia"] * case.n_nodes)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits", "-lms", "100"],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference(cfg: str, steps: int, warmup: int, ref_n: int, threads: int = 0):
+    """The unmodified reference on a bounded sample of the workload (same generator, smaller n)."""
+    from oracle import oracle as O
+    from paper_2303_02156_b200 import configs as C
+    if not os.path.exists(O.REF_DRIVER):
+        return None, "oracle/_ref/ref_driver not built"
+    n = ref_n or {"c1": 20, "c2": 40, "c3": 16, "c4": 300, "c5": 30}[cfg]
+    if cfg == "c1":
+        case = C.config1(n)
+    elif cfg == "c2":
+        case = C.config2(n)
+    elif cfg == "c3":
+        case = C.config3(n)
+    elif cfg == "c4":
+        case = C.config4(n)
+    else:
+        case = C.config5(n, 4 * (n + 1) ** 3)
+    d = tempfile.mkdtemp(prefix="symel_refbench_")
+    try:
+        case.write_case_dir(d)
+        threads = threads or os.cpu_count() or 1
+        info = O.run_ref_driver(d, backend="source", threads=threads, lanes=8, repeat=max(1, steps), dump=False,
+                                cache=os.path.join(d, "kcache"))
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    melem = info["n_elements"] / (info["mean_ms"] * 1e-3) / 1e6
+    sample = (f"{cfg} generator at n={n}: {info['n_elements']} elements; reference Assembler::assemble "
+              f"(source backend, lanes 8, {threads} threads), mean of {steps} steady-state calls after "
+              f"1 warm-up (first call {info['first_ms']:.0f} ms incl. kernel compile + pattern build); no SPD "
+              f"(the reference has none)")
+    return {"value": melem, "unit": "M elements/s", "cores": threads, "kind": "reference", "sample": sample,
+            "ms_per_assemble": info["mean_ms"], "eval_ms": info["eval_ms"], "assemble_ms": info["assemble_ms"]}, None
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    meta = config_meta(args.config)
+    spd = meta["spd"] and not args.no_spd
+    metric = "M elements/s for energy+grad+Hessian+BSR assembly"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        base, why = cpu_reference(args.config, args.steps, args.warmup, args.ref_n)
+        if base is None:
+            print(json.dumps({"impl": "reference", "unavailable": why}))
+            return 0
+        line = {"impl": "reference", "metric": metric, "value": base["value"], "unit": "M elements/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": base["ms_per_assemble"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, bounded sample)",
+                "config": {"workload": meta["workload"], "sample": base["sample"]},
+                "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": base["value"], "unit": "M elements/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+
+    from paper_2303_02156_b200.systems import DeviceSystem
+
+    case = make_case(args.config)
+    ds = DeviceSystem(case, spd=spd, device=local)
+    A = ds.asm
+    stream = torch.cuda.ExternalStream(A.stream(), device=local)
+    n_elem = case.n_elements()
+    t_setup = time.time()
+    for _ in range(max(3, args.warmup)):
+        A.assemble(args.mode)
+    setup_s = time.time() - t_setup
+    tm = A.timings()
+
+    # ---- device-resident timed region
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = A.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eval_ms = []
+    for _ in range(args.steps):
+        A.assemble(args.mode)
+        eval_ms.append(A.timings().eval_ms)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    launches = (A.launch_count() - l0) // max(1, args.steps)
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n_elem / (ms * 1e-3) / 1e6
+
+    # ---- roofline of the dominant kernel (element eval + fused assembly)
+    fl = flops_per_step(args.config, case)
+    k_ms = float(np.mean(eval_ms))
+    peak = A.fp64_peak_tflops()
+    achieved = fl / (k_ms * 1e-3) / 1e12
+    roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel_ms": k_ms, "kernel_share_of_step": k_ms / ms,
+            "peak_source": "measured DFMA probe on this GPU (symel_cuda_fp64_peak)",
+            "algorithmic_flops_per_step": fl}
+
+    # ---- end to end through the C ABI with host buffers: H2D x, assemble, D2H E + gradient
+    x_host = torch.empty(case.x.size, dtype=torch.float64, pin_memory=True)
+    x_host.numpy()[:] = case.x.ravel()
+    g_host = torch.empty(case.x.size, dtype=torch.float64, pin_memory=True)
+    import ctypes
+    lib = A.lib
+    torch.cuda.synchronize()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        lib.symel_cuda_set_array(A.h, ds.x, ctypes.c_void_p(x_host.data_ptr()), case.x.size)
+        E = A.assemble(args.mode)
+        lib.symel_cuda_copy_gradient(A.h, ctypes.c_void_p(g_host.data_ptr()))
+    e3.record(stream)
+    e3.synchronize()
+    e2e_ms = e2.elapsed_time(e3) / args.steps
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": world * n_elem / (e2e_ms * 1e-3) / 1e6, "unit": "M elements/s",
+           "h2d_bytes_per_step": int(case.x.size * 8), "d2h_bytes_per_step": int(case.x.size * 8 + 8),
+           "ms_per_step": e2e_ms, "note": "BSR values stay device-resident for the device PCG consumer"}
+
+    line = {"metric": metric, "value": value, "unit": "M elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE shapes)",
+            "config": {"workload": meta["workload"], "elements": n_elem, "mode": args.mode, "spd": spd,
+                       "parallelism": f"replicas{world}",
+                       "l2": "working set (BSR values + slot maps + connectivity) >> 126 MB L2; no flush needed",
+                       "pattern_ms": tm.pattern_ms, "compile_ms": tm.compile_ms, "setup_s": setup_s},
+            "roofline": roof, "clocks": clk, "e2e": e2e, "gpu_launches": int(launches)}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base, why = cpu_reference(args.config, 3, 1, args.ref_n)
+        line["cpu_baseline"] = base if base else {"unavailable": why}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,502 @@
+// Static sm_100a kernels of the device assembly path (everything that is not generated
+// from a tape): sparsity pattern + element->slot maps (replaces build_pattern,
+// assembly.hpp:271-375), the reference-order scatter (assembly.hpp:450-462), energy sums and
+// the finiteness reduction (assembly.hpp:426-448), activation compaction and guard minimum
+// (assembly.hpp:143-173, 227-261), and pins (assembly.hpp:464-489).
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <limits>
+
+#include "device_ops.hpp"
+
+namespace symel_cuda::dev {
+
+namespace {
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+template <class T>
+int dalloc(T** p, size_t n, void* s) {
+  return (int)cudaMallocAsync((void**)p, sizeof(T) * (n ? n : 1), S(s));
+}
+
+int bits_for(unsigned long long v) {
+  int b = 1;
+  while (b < 64 && (1ull << b) <= v) ++b;
+  return b;
+}
+
+__device__ __forceinline__ long long lb_block(const LbDesc& d, const int* tup, int q) {
+  return (d.off[q] + (long long)tup[d.slot[q]] * d.comps[q]) / d.b;
+}
+
+__global__ void k_pattern_keys(LbDesc d, const int* __restrict__ conn, const int* __restrict__ active,
+                               long long n, unsigned long long* __restrict__ keys,
+                               unsigned long long* counter) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long e = active ? active[t] : t;
+  const int* tup = conn + e * d.arity;
+  long long blk[kMaxLb];
+  for (int q = 0; q < d.n_lb; ++q) blk[q] = lb_block(d, tup, q);
+  int cnt = 0;
+  for (int i = 0; i < d.n_lb; ++i)
+    for (int j = 0; j < d.n_lb; ++j) cnt += blk[i] != blk[j];
+  unsigned long long pos = atomicAdd(counter, (unsigned long long)cnt);
+  for (int i = 0; i < d.n_lb; ++i)
+    for (int j = 0; j < d.n_lb; ++j)
+      if (blk[i] != blk[j]) keys[pos++] = ((unsigned long long)blk[i] << 32) | (unsigned long long)blk[j];
+}
+
+__global__ void k_diag_keys(long long n, unsigned long long* keys) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) keys[r] = ((unsigned long long)r << 32) | (unsigned long long)r;
+}
+
+__global__ void k_row_ptr(const unsigned long long* __restrict__ keys, long long nk, long long n_rows,
+                          int* __restrict__ row_ptr, int* __restrict__ col_idx) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nk) {
+    const unsigned long long k = keys[i];
+    col_idx[i] = (int)(k & 0xffffffffull);
+    const long long r = (long long)(k >> 32);
+    const long long pr = i == 0 ? -1 : (long long)(keys[i - 1] >> 32);
+    for (long long q = pr + 1; q <= r; ++q) row_ptr[q] = (int)i;  // rows start here
+    if (i == nk - 1)
+      for (long long q = r + 1; q <= n_rows; ++q) row_ptr[q] = (int)nk;
+  }
+}
+
+__device__ __forceinline__ int find_block(const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+                                          long long r, long long c) {
+  int lo = row_ptr[r], hi = row_ptr[r + 1];
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (col_idx[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_slot_map(LbDesc d, const int* __restrict__ conn, const int* __restrict__ active, long long n,
+                           const int* __restrict__ row_ptr, const int* __restrict__ col_idx, int* __restrict__ slots) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long e = active ? active[t] : t;
+  const int* tup = conn + e * d.arity;
+  long long blk[kMaxLb];
+  for (int q = 0; q < d.n_lb; ++q) blk[q] = lb_block(d, tup, q);
+  int* out = slots + t * d.n_lb * d.n_lb;
+  for (int i = 0; i < d.n_lb; ++i)
+    for (int j = 0; j < d.n_lb; ++j) out[i * d.n_lb + j] = find_block(row_ptr, col_idx, blk[i], blk[j]);
+}
+
+__global__ void k_refs(const int* __restrict__ slots, const int* __restrict__ conn, const int* __restrict__ active,
+                       long long n, long long ord_base, LbDesc d, unsigned long long pos_h, unsigned long long pos_g,
+                       unsigned* __restrict__ hkey, unsigned long long* __restrict__ hval, unsigned* __restrict__ gkey,
+                       unsigned long long* __restrict__ gval) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long e = active ? active[t] : t;
+  const int* tup = conn + e * d.arity;
+  const int nl = d.n_lb;
+  const unsigned long long ord = (unsigned long long)(ord_base + t);
+  for (int i = 0; i < nl; ++i) {
+    gkey[pos_g + t * nl + i] = (unsigned)lb_block(d, tup, i);
+    gval[pos_g + t * nl + i] = (ord << 5) | (unsigned long long)i;
+    for (int j = 0; j < nl; ++j) {
+      const long long q = pos_h + (t * nl + i) * nl + j;
+      hkey[q] = (unsigned)slots[(t * nl + i) * nl + j];
+      hval[q] = (ord << 10) | ((unsigned long long)i << 5) | (unsigned long long)j;
+    }
+  }
+}
+
+__global__ void k_seg_ptr(const unsigned* __restrict__ keys, long long nk, long long nseg, int* __restrict__ ptr) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nk) {
+    const long long r = keys[i];
+    const long long pr = i == 0 ? -1 : (long long)keys[i - 1];
+    for (long long q = pr + 1; q <= r; ++q) ptr[q] = (int)i;
+    if (i == nk - 1)
+      for (long long q = r + 1; q <= nseg; ++q) ptr[q] = (int)nk;
+  }
+  if (nk == 0 && i <= nseg) ptr[i] = 0;
+}
+
+struct LayoutTable {
+  ContribLayout e[8];
+  int n;
+};
+
+__device__ __forceinline__ const ContribLayout& which(const LayoutTable& L, unsigned long long ord) {
+  int k = 0;
+  while (k + 1 < L.n && (long long)ord >= L.e[k].ord_end) ++k;
+  return L.e[k];
+}
+
+// One thread per BSR block: contributions in ascending (energy, element, a, c) order from +0.0.
+__global__ void k_ordered_hess(LayoutTable L, const int* __restrict__ ptr, const unsigned long long* __restrict__ ref,
+                               long long n_blocks, int b, double* __restrict__ vals) {
+  const long long blk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (blk >= n_blocks) return;
+  double acc[9];
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+  for (int k = ptr[blk]; k < ptr[blk + 1]; ++k) {
+    const unsigned long long r = ref[k];
+    const unsigned long long ord = r >> 10;
+    const int li = (int)((r >> 5) & 31), lj = (int)(r & 31);
+    const ContribLayout& c = which(L, ord);
+    const double* src = c.contrib + (long long)(ord - c.ord_base) * c.stride + 1 + c.n_dofs;
+    for (int ri = 0; ri < b; ++ri) {
+      const int di = c.dof_of[li * 3 + ri];
+      if (di < 0) continue;
+      for (int rj = 0; rj < b; ++rj) {
+        const int dj = c.dof_of[lj * 3 + rj];
+        if (dj < 0) continue;
+        acc[ri * b + rj] += src[di * c.n_dofs + dj];
+      }
+    }
+  }
+  for (int q = 0; q < b * b; ++q) vals[blk * b * b + q] = acc[q];
+}
+
+__global__ void k_ordered_grad(LayoutTable L, const int* __restrict__ ptr, const unsigned long long* __restrict__ ref,
+                               long long n_rows, int b, double* __restrict__ grad) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n_rows) return;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int k = ptr[row]; k < ptr[row + 1]; ++k) {
+    const unsigned long long r = ref[k];
+    const unsigned long long ord = r >> 5;
+    const int li = (int)(r & 31);
+    const ContribLayout& c = which(L, ord);
+    const double* src = c.contrib + (long long)(ord - c.ord_base) * c.stride + 1;
+    for (int q = 0; q < b; ++q) {
+      const int d = c.dof_of[li * 3 + q];
+      if (d >= 0) acc[q] += src[d];
+    }
+  }
+  for (int q = 0; q < b; ++q) grad[row * b + q] = acc[q];
+}
+
+__global__ void k_gather_strided(const double* __restrict__ src, long long stride, long long n, double* __restrict__ dst) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i * stride];
+}
+
+__global__ void k_serial_sum(const double* __restrict__ v, long long n, double init_from, double* out, int accumulate) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double e = accumulate ? *out : 0.0;
+  for (long long i = 0; i < n; ++i) e += v[i];
+  *out = e;
+  (void)init_from;
+}
+
+constexpr int kTreeChunk = 4096;  // fixed reduction shape => result independent of launch size
+constexpr int kTreeThreads = 256;
+
+__global__ void k_tree_partial(const double* __restrict__ v, long long stride, long long n, double* __restrict__ partial) {
+  __shared__ double sh[kTreeThreads];
+  const long long base = (long long)blockIdx.x * kTreeChunk;
+  double s = 0.0;
+  for (int q = 0; q < kTreeChunk / kTreeThreads; ++q) {
+    const long long i = base + (long long)q * kTreeThreads + threadIdx.x;
+    if (i < n) s += v[i * stride];
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kTreeThreads / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_tree_final(const double* __restrict__ partial, long long n, double* out) {
+  __shared__ double sh[kTreeThreads];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += kTreeThreads) s += partial[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kTreeThreads / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void k_combine(const double* __restrict__ v, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double e = 0.0;
+    for (int i = 0; i < n; ++i) e += v[i];
+    *out = e;
+  }
+}
+
+__global__ void k_act_mask(const double* __restrict__ v, long long n, int kind, unsigned char* __restrict__ mask,
+                           int* changed) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = v[i];
+  const unsigned char a = kind == 0 ? (x >= 0.0) : (x > 0.0);  // Condition::holds, expr.hpp:574
+  if (a != mask[i]) {
+    mask[i] = a;
+    *changed = 1;
+  }
+}
+
+struct MinOp {
+  __device__ __forceinline__ double operator()(double a, double b) const { return b < a ? b : a; }
+};
+
+__global__ void k_pins(const unsigned char* __restrict__ mask, long long n_rows, int b, const int* __restrict__ row_ptr,
+                       const int* __restrict__ col_idx, double* __restrict__ vals, double* __restrict__ grad) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  for (int q = 0; q < b; ++q)
+    if (mask[r * b + q]) grad[r * b + q] = 0.0;
+  for (int k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+    const long long c = col_idx[k];
+    double* v = vals + (long long)k * b * b;
+    for (int i = 0; i < b; ++i) {
+      const bool pr = mask[r * b + i] != 0;
+      for (int j = 0; j < b; ++j)
+        if (pr || mask[c * b + j]) v[i * b + j] = 0.0;
+    }
+    if (c == r)
+      for (int i = 0; i < b; ++i)
+        if (mask[r * b + i]) v[i * b + i] = 1.0;
+  }
+}
+
+inline unsigned grid_for(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// FP64 pipe peak probe: 8 independent DFMA chains per thread (enough ILP for full issue).
+__global__ void __launch_bounds__(256) k_dfma_peak(int iters, double b, double c, double* sink) {
+  double a[8];
+  for (int q = 0; q < 8; ++q) a[q] = threadIdx.x * 1e-9 + q;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = fma(a[q], b, c);
+  double s = 0;
+  for (int q = 0; q < 8; ++q) s += a[q];
+  if (s == 123.456) *sink = s;
+}
+
+}  // namespace
+
+int fp64_peak(int n_sm, double* tflops, void* s) {
+  double* sink;
+  int err;
+  if ((err = dalloc(&sink, 1, s))) return err;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 1 << 14, blocks = n_sm * 8, threads = 256;
+  k_dfma_peak<<<blocks, threads, 0, S(s)>>>(64, 0.999999, 1e-7, sink);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, S(s));
+    k_dfma_peak<<<blocks, threads, 0, S(s)>>>(iters, 0.999999, 1e-7, sink);
+    cudaEventRecord(e1, S(s));
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  *tflops = 2.0 * 8.0 * iters * (double)blocks * threads / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(sink, S(s));
+  return (int)cudaGetLastError();
+}
+
+int pattern_keys(const LbDesc& d, const int* conn, const int* active, long long n, unsigned long long* keys,
+                 unsigned long long* counter, void* s) {
+  if (n <= 0) return 0;
+  k_pattern_keys<<<grid_for(n, 256), 256, 0, S(s)>>>(d, conn, active, n, keys, counter);
+  return (int)cudaGetLastError();
+}
+
+int diag_keys(long long n_rows, unsigned long long* keys, void* s) {
+  if (n_rows <= 0) return 0;
+  k_diag_keys<<<grid_for(n_rows, 256), 256, 0, S(s)>>>(n_rows, keys);
+  return (int)cudaGetLastError();
+}
+
+int build_csr(unsigned long long* keys, long long nk, long long n_rows, int** row_ptr, int** col_idx,
+              long long* n_blocks, void* s) {
+  int err;
+  unsigned long long* sorted = nullptr;
+  if ((err = dalloc(&sorted, nk, s))) return err;
+  const int end_bit = 32 + bits_for((unsigned long long)n_rows);
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, sorted, nk, 0, end_bit, S(s));
+  void* tmp = nullptr;
+  if ((err = dalloc((char**)&tmp, tmp_bytes, s))) return err;
+  cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, nk, 0, end_bit, S(s));
+  cudaFreeAsync(tmp, S(s));
+  long long* d_nu = nullptr;
+  if ((err = dalloc(&d_nu, 1, s))) return err;
+  tmp_bytes = 0;
+  cub::DeviceSelect::Unique(nullptr, tmp_bytes, sorted, keys, d_nu, nk, S(s));
+  if ((err = dalloc((char**)&tmp, tmp_bytes, s))) return err;
+  cub::DeviceSelect::Unique(tmp, tmp_bytes, sorted, keys, d_nu, nk, S(s));
+  cudaFreeAsync(tmp, S(s));
+  cudaFreeAsync(sorted, S(s));
+  long long nu = 0;
+  cudaMemcpyAsync(&nu, d_nu, sizeof nu, cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  cudaFreeAsync(d_nu, S(s));
+  if (nu >= (1ll << 31)) return (int)cudaErrorInvalidValue;
+  if ((err = dalloc(row_ptr, n_rows + 1, s))) return err;
+  if ((err = dalloc(col_idx, nu, s))) return err;
+  k_row_ptr<<<grid_for(nu, 256), 256, 0, S(s)>>>(keys, nu, n_rows, *row_ptr, *col_idx);
+  *n_blocks = nu;
+  return (int)cudaGetLastError();
+}
+
+int slot_map(const LbDesc& d, const int* conn, const int* active, long long n, const int* row_ptr,
+             const int* col_idx, int* slots, void* s) {
+  if (n <= 0) return 0;
+  k_slot_map<<<grid_for(n, 128), 128, 0, S(s)>>>(d, conn, active, n, row_ptr, col_idx, slots);
+  return (int)cudaGetLastError();
+}
+
+int ordered_refs(const EnergyRefSrc* src, int ne, long long n_blocks, long long n_rows, OrderedRefs* out,
+                 void* s) {
+  int err;
+  long long nh = 0, ng = 0;
+  for (int k = 0; k < ne; ++k) {
+    nh += src[k].n_active * src[k].d.n_lb * src[k].d.n_lb;
+    ng += src[k].n_active * src[k].d.n_lb;
+  }
+  unsigned *hk, *gk, *hk2, *gk2;
+  unsigned long long *hv, *gv, *hv2, *gv2;
+  if ((err = dalloc(&hk, nh, s)) || (err = dalloc(&hv, nh, s)) || (err = dalloc(&gk, ng, s)) ||
+      (err = dalloc(&gv, ng, s)) || (err = dalloc(&hk2, nh, s)) || (err = dalloc(&hv2, nh, s)) ||
+      (err = dalloc(&gk2, ng, s)) || (err = dalloc(&gv2, ng, s)))
+    return err;
+  unsigned long long ph = 0, pg = 0;
+  for (int k = 0; k < ne; ++k) {
+    const EnergyRefSrc& e = src[k];
+    if (e.n_active > 0)
+      k_refs<<<grid_for(e.n_active, 128), 128, 0, S(s)>>>(e.slots, e.conn, e.active, e.n_active, e.ord_base, e.d,
+                                                          ph, pg, hk, hv, gk, gv);
+    ph += (unsigned long long)e.n_active * e.d.n_lb * e.d.n_lb;
+    pg += (unsigned long long)e.n_active * e.d.n_lb;
+  }
+  // stable LSD radix sort keeps the generation order (energy, element, a, c) per key
+  size_t tb = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, hk2, hv, hv2, nh, 0, bits_for(n_blocks), S(s));
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, gk, gk2, gv, gv2, ng, 0, bits_for(n_rows), S(s));
+  void* tmp;
+  if ((err = dalloc((char**)&tmp, tb > tb2 ? tb : tb2, s))) return err;
+  cub::DeviceRadixSort::SortPairs(tmp, tb, hk, hk2, hv, hv2, nh, 0, bits_for(n_blocks), S(s));
+  tb2 = tb > tb2 ? tb : tb2;
+  cub::DeviceRadixSort::SortPairs(tmp, tb2, gk, gk2, gv, gv2, ng, 0, bits_for(n_rows), S(s));
+  cudaFreeAsync(tmp, S(s));
+  if ((err = dalloc(&out->hess_ptr, n_blocks + 1, s)) || (err = dalloc(&out->grad_ptr, n_rows + 1, s))) return err;
+  k_seg_ptr<<<grid_for(nh > n_blocks + 1 ? nh : n_blocks + 1, 256), 256, 0, S(s)>>>(hk2, nh, n_blocks, out->hess_ptr);
+  k_seg_ptr<<<grid_for(ng > n_rows + 1 ? ng : n_rows + 1, 256), 256, 0, S(s)>>>(gk2, ng, n_rows, out->grad_ptr);
+  cudaFreeAsync(hk, S(s)); cudaFreeAsync(hv, S(s)); cudaFreeAsync(gk, S(s)); cudaFreeAsync(gv, S(s));
+  cudaFreeAsync(hk2, S(s)); cudaFreeAsync(gk2, S(s));
+  out->hess_ref = hv2;
+  out->grad_ref = gv2;
+  out->n_hess = nh;
+  out->n_grad = ng;
+  return (int)cudaGetLastError();
+}
+
+void free_ordered_refs(OrderedRefs* r) {
+  cudaFree(r->hess_ptr); cudaFree(r->hess_ref); cudaFree(r->grad_ptr); cudaFree(r->grad_ref);
+  *r = OrderedRefs{};
+}
+
+int ordered_scatter(const ContribLayout* lay, int ne, const OrderedRefs& r, long long n_blocks, long long n_rows,
+                    double* vals, double* grad, void* s) {
+  if (ne > 8) return (int)cudaErrorInvalidValue;
+  LayoutTable L{};
+  L.n = ne;
+  for (int k = 0; k < ne; ++k) L.e[k] = lay[k];
+  const int b = lay[0].b;
+  if (n_blocks > 0) k_ordered_hess<<<grid_for(n_blocks, 128), 128, 0, S(s)>>>(L, r.hess_ptr, r.hess_ref, n_blocks, b, vals);
+  if (n_rows > 0) k_ordered_grad<<<grid_for(n_rows, 128), 128, 0, S(s)>>>(L, r.grad_ptr, r.grad_ref, n_rows, b, grad);
+  return (int)cudaGetLastError();
+}
+
+int energy_serial(const double* const* elemE, const long long* strides, const long long* counts, int ne,
+                  double* out, void* s) {
+  long long mx = 0;
+  for (int k = 0; k < ne; ++k) mx = counts[k] > mx ? counts[k] : mx;
+  double* tmp;
+  int err;
+  if ((err = dalloc(&tmp, mx, s))) return err;
+  cudaMemsetAsync(out, 0, sizeof(double), S(s));
+  for (int k = 0; k < ne; ++k) {
+    if (counts[k] == 0) continue;
+    k_gather_strided<<<grid_for(counts[k], 256), 256, 0, S(s)>>>(elemE[k], strides[k], counts[k], tmp);
+    k_serial_sum<<<1, 32, 0, S(s)>>>(tmp, counts[k], 0.0, out, 1);
+  }
+  cudaFreeAsync(tmp, S(s));
+  return (int)cudaGetLastError();
+}
+
+int energy_tree(const double* v, long long stride, long long n, double* partial, double* out, void* s) {
+  if (n == 0) return (int)cudaMemsetAsync(out, 0, sizeof(double), S(s));
+  const long long nb = (n + kTreeChunk - 1) / kTreeChunk;
+  k_tree_partial<<<(unsigned)nb, kTreeThreads, 0, S(s)>>>(v, stride, n, partial);
+  k_tree_final<<<1, kTreeThreads, 0, S(s)>>>(partial, nb, out);
+  return (int)cudaGetLastError();
+}
+
+long long energy_tree_partials(long long n) { return (n + kTreeChunk - 1) / kTreeChunk; }
+
+int energy_combine(const double* per_energy, int n, double* out, void* s) {
+  k_combine<<<1, 32, 0, S(s)>>>(per_energy, n, out);
+  return (int)cudaGetLastError();
+}
+
+int activation_mask(const double* v, long long n, int kind, unsigned char* mask, int* changed, void* s) {
+  if (n <= 0) return 0;
+  k_act_mask<<<grid_for(n, 256), 256, 0, S(s)>>>(v, n, kind, mask, changed);
+  return (int)cudaGetLastError();
+}
+
+int compact_active(const unsigned char* mask, long long n, int* active, long long* n_active_host, void* s) {
+  int err;
+  long long* d_n;
+  if ((err = dalloc(&d_n, 1, s))) return err;
+  size_t tb = 0;
+  cub::CountingInputIterator<int> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tb, it, mask, active, d_n, n, S(s));
+  void* tmp;
+  if ((err = dalloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceSelect::Flagged(tmp, tb, it, mask, active, d_n, n, S(s));
+  cudaMemcpyAsync(n_active_host, d_n, sizeof(long long), cudaMemcpyDeviceToHost, S(s));
+  cudaFreeAsync(tmp, S(s));
+  cudaFreeAsync(d_n, S(s));
+  return (int)cudaStreamSynchronize(S(s));
+}
+
+int min_reduce(const double* v, long long n, double* out, void* s) {
+  size_t tb = 0;
+  cub::DeviceReduce::Reduce(nullptr, tb, v, out, n, MinOp(), std::numeric_limits<double>::infinity(), S(s));
+  void* tmp;
+  int err;
+  if ((err = dalloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceReduce::Reduce(tmp, tb, v, out, n, MinOp(), std::numeric_limits<double>::infinity(), S(s));
+  cudaFreeAsync(tmp, S(s));
+  return (int)cudaGetLastError();
+}
+
+int apply_pins(const unsigned char* mask, long long n_rows, int b, const int* row_ptr, const int* col_idx,
+               double* vals, double* grad, void* s) {
+  if (n_rows <= 0) return 0;
+  k_pins<<<grid_for(n_rows, 128), 128, 0, S(s)>>>(mask, n_rows, b, row_ptr, col_idx, vals, grad);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace symel_cuda::dev

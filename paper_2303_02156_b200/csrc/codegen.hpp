@@ -1,0 +1,77 @@
+// CUDA backend of the code generator: emits one specialised sm_100a kernel per energy tape.
+//
+// Replaces the reference's C++ emitter (`emit_kernel_source`, kernel.hpp:47-97) for the
+// device: the same Tape IR is lowered to a thread-per-element kernel whose gather
+// (registry.hpp:261-287 `gather_element_inputs`) is specialised on the input binding, whose
+// instruction order is rescheduled for register pressure, and whose outputs are either
+// stored in the reference's per-element layout (`contrib_`, assembly.hpp:377-424) or fused
+// straight into the assembly (gradient + 3x3 BSR).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tape_io.hpp"
+
+namespace symel_cuda {
+
+inline constexpr int kMaxArrays = 24;
+inline constexpr int kMaxParams = 32;
+
+// detail::InputKind (registry.hpp:54-59)
+enum class InKind : std::uint32_t { item_comp = 0, elem_comp = 1, param = 2, sum_comp = 3 };
+
+struct InputBinding {
+  InKind kind = InKind::item_comp;
+  std::uint32_t array = 0;       // array id (item_comp / elem_comp)
+  std::uint32_t tuple_slot = 0;  // connectivity slot (item_comp) / item column (sum_comp)
+  std::uint32_t comp = 0;
+};
+
+enum class OutMode : std::uint32_t {
+  contrib = 0,   // reference layout [E, g(n), H(n*n)] per active element (exact order path)
+  fused_atomic,  // E per element; g and BSR via red.global.add.f64 (nondeterministic order)
+  fused_tile,    // E per element; g / BSR entries to per-element staging for the tile reducer
+  value_only,    // activation / guard kernels: single output per element (+ item reduction)
+};
+
+struct KernelSpec {
+  const TapeIR* tape = nullptr;
+  std::vector<InputBinding> inputs;      // one per tape input slot
+  std::vector<std::uint32_t> dof_slots;  // input slots that are dofs, bind order
+  std::vector<std::uint32_t> array_comps;  // comps per array id
+  std::uint32_t arity = 1;
+  std::vector<double> sum_items;         // n_items x sum_arity, row-major (fixed summation)
+  std::uint32_t n_items = 0, sum_arity = 0;
+  std::uint32_t b = 3;                   // BSR block size (assembly.hpp:273-276)
+  OutMode mode = OutMode::contrib;
+  bool fast = true;        // division strength reduction + FMA contraction
+  bool spd = false;        // per-element SPD projection of the element Hessian (new, K2)
+  int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)
+  int schedule = 1;        // 0 = tape order, 1 = output-driven DFS (register-pressure aware)
+  int threads_per_block = 128;
+  int min_blocks = 2;
+  std::string name = "sy_kernel";
+};
+
+// Derived facts about the element's dof -> block mapping (fused modes).
+struct BlockMap {
+  std::uint32_t n_lb = 0;                 // local blocks per element
+  std::vector<std::uint32_t> lb_of_dof;   // per dof (bind order)
+  std::vector<std::uint32_t> entry_of_dof;
+  std::vector<std::uint32_t> lb_array, lb_slot, lb_comp0;  // per local block: source item
+};
+
+BlockMap make_block_map(const KernelSpec& spec);
+
+// Shared declarations (argument struct) prepended to every generated kernel and used by
+// the host launcher; layout must stay identical on both sides.
+const char* kernel_prelude();
+
+std::string emit_kernel(const KernelSpec& spec);
+
+// Instruction order used for emission (indices into tape->instrs).
+std::vector<std::uint32_t> schedule_instrs(const TapeIR& t, int schedule);
+
+}  // namespace symel_cuda

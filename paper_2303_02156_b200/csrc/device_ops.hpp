@@ -1,0 +1,112 @@
+// Host-callable wrappers around the static sm_100a kernels in assembly_kernels.cu.
+// All functions enqueue on `stream` and return cudaError_t as int (0 = success).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace symel_cuda::dev {
+
+inline constexpr int kMaxLb = 32;  // local blocks per element (tet10: 10, pairs: 4)
+
+// Local block descriptors of one energy (see codegen BlockMap): block of an element's local
+// block q = (set_off[array[q]] + item * comps[array[q]] + comp0[q]) / b, item = conn[slot[q]].
+struct LbDesc {
+  int n_lb;
+  int b;
+  int arity;
+  int slot[kMaxLb];
+  long long off[kMaxLb];    // set offset + comp0 of the owning dof array
+  int comps[kMaxLb];
+};
+
+// --- pattern (replaces build_pattern, assembly.hpp:271-375) ---------------------------
+// Emits 64-bit keys (row << 32 | col) for every off-diagonal local block pair of every active
+// element; returns the count written at keys + *n_out (device counter).
+int pattern_keys(const LbDesc& d, const int* conn, const int* active, long long n_active,
+                 unsigned long long* keys, unsigned long long* counter, void* stream);
+int diag_keys(long long n_rows, unsigned long long* keys, void* stream);
+// Sorts + uniques keys in place; builds row_ptr (n_rows+1) / col_idx; returns n_blocks.
+int build_csr(unsigned long long* keys, long long n_keys, long long n_rows, int** row_ptr,
+              int** col_idx, long long* n_blocks, void* stream);
+// Slot map: per active element, n_lb*n_lb block ordinals (row-major over local blocks).
+int slot_map(const LbDesc& d, const int* conn, const int* active, long long n_active,
+             const int* row_ptr, const int* col_idx, int* slots, void* stream);
+
+// --- ordered (reference-order) scatter, assembly.hpp:327-374 + 450-462 -----------------
+// Builds per-block and per-row contribution lists in ascending (energy, element, a, c) order.
+struct OrderedRefs {
+  long long n_hess = 0, n_grad = 0;
+  int* hess_ptr = nullptr;             // n_blocks + 1
+  unsigned long long* hess_ref = nullptr;  // (contrib element ordinal << 10) | (li << 5) | lj
+  int* grad_ptr = nullptr;             // n_rows + 1
+  unsigned long long* grad_ref = nullptr;  // (contrib element ordinal << 5) | li
+};
+struct EnergyRefSrc {
+  const int* slots;      // per active element n_lb^2
+  const int* conn;
+  const int* active;
+  long long n_active;
+  long long ord_base;    // first global contrib ordinal of this energy
+  LbDesc d;
+};
+int ordered_refs(const EnergyRefSrc* src, int n_energies, long long n_blocks, long long n_rows,
+                 OrderedRefs* out, void* stream);
+void free_ordered_refs(OrderedRefs* r);
+
+// Per energy: contrib row stride and the (lb, entry) -> dof index table (-1 = absent).
+struct ContribLayout {
+  long long ord_base;  // first element ordinal (global over energies) of the energy
+  long long ord_end;
+  const double* contrib;  // this energy's contrib block (stride doubles per element)
+  int stride;
+  int n_dofs;
+  int n_lb;
+  int b;
+  signed char dof_of[kMaxLb * 3];
+};
+int ordered_scatter(const ContribLayout* lay, int n_energies, const OrderedRefs& r, long long n_blocks,
+                    long long n_rows, double* vals, double* grad, void* stream);
+
+// --- energy and finiteness (assembly.hpp:426-448) ---------------------------------------
+// serial sum in (energy, element) order -- exact reference order, one thread
+int energy_serial(const double* const* elemE, const long long* strides, const long long* counts,
+                  int n_energies, double* out, void* stream);
+// deterministic fixed-shape tree sum of n values (strided)
+int energy_tree(const double* v, long long stride, long long n, double* partial, double* out, void* stream);
+long long energy_tree_partials(long long n);
+// combine per-energy totals in energy order (out = ((0 + e0) + e1) + ...)
+int energy_combine(const double* per_energy, int n, double* out, void* stream);
+
+// --- activation / guard (assembly.hpp:143-173, 227-261) ---------------------------------
+int activation_mask(const double* v, long long n, int kind, unsigned char* mask, int* changed,
+                    void* stream);
+int compact_active(const unsigned char* mask, long long n, int* active, long long* n_active_host,
+                   void* stream);
+int min_reduce(const double* v, long long n, double* out, void* stream);
+
+// --- measurement: FP64 DFMA throughput (TFLOP/s, FMA = 2 flops) over the whole device
+int fp64_peak(int n_sm, double* tflops, void* stream);
+
+// --- pins (assembly.hpp:464-489) -----------------------------------------------------------
+int apply_pins(const unsigned char* mask, long long n_rows, int b, const int* row_ptr, const int* col_idx,
+               double* vals, double* grad, void* stream);
+
+// --- tile-deterministic reduction (K3) ------------------------------------------------------
+// see assembly_kernels.cu for the plan layout
+struct TilePlan {
+  int tile;                 // elements per tile
+  long long n_tiles;
+  int* blk_ptr = nullptr;   // per tile: [start of its unique block list] (n_tiles + 1)
+  int* blk_id = nullptr;    // unique global block ordinals per tile (sorted)
+  int* blk_dst = nullptr;   // >= 0: final block (write directly); < 0: -(partial index)-1
+  int* con_ptr = nullptr;   // per (tile, unique block): contribution range (absolute)
+  unsigned* con = nullptr;  // (element-in-tile << 10) | (li << 5) | lj
+  long long n_partials = 0;
+  int* part_ptr = nullptr;  // per boundary block: range of partial indices (in tile order)
+  int* part_blk = nullptr;  // boundary blocks
+  int* part_idx = nullptr;
+  long long n_part_blocks = 0;
+};
+
+}  // namespace symel_cuda::dev

@@ -1,0 +1,1124 @@
+// libsymel_cuda.so: implementation of the C ABI in include/symel_cuda.h.
+//
+// Device-side replacement for the body of Assembler::assemble (assembly.hpp:108-126):
+// prepare/compile (registry.hpp:620-653) -> NVRTC-compiled sm_100a kernels generated from the
+// reference's Tape IR; refresh_activation + build_pattern -> device kernels; evaluate_active +
+// check_finite + sum_energy + scatter + apply_pins -> device kernels. No CPU fallback: without
+// a CUDA device every compute entry point fails with SYMEL_E_NODEVICE.
+#include "../../include/symel_cuda.h"
+
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "codegen.hpp"
+#include "device_ops.hpp"
+#include "sy_args.h"
+#include "tape_io.hpp"
+
+using namespace symel_cuda;
+
+namespace {
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(expr)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (cudaError_t)(expr);                                                   \
+    if (e_ != cudaSuccess) throw Fail{SYMEL_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+std::uint64_t fnv1a(const std::string& s) {
+  std::uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+struct Compiled {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kernel = nullptr;
+  int tpb = 128;
+  std::string source;
+};
+
+// Kernel variants per energy.
+enum Variant : int {
+  V_CONTRIB_IEEE = 0,
+  V_CONTRIB_FAST,
+  V_ATOMIC,
+  V_ENERGY,  // E only (fast), line-search probe
+  V_ACT,
+  V_GUARD,
+  V_TILE,
+  V_COUNT
+};
+
+struct Array {
+  std::string name;
+  std::uint64_t items = 0;
+  std::uint32_t comps = 0;
+  bool is_dof = false;
+  double* d = nullptr;
+};
+
+struct Conn {
+  std::string name;
+  std::uint32_t arity = 0;
+  std::uint64_t n = 0;
+  int* d = nullptr;
+};
+
+struct Energy {
+  std::string name;
+  int conn = -1;
+  TapeIR deriv, act, guard, eonly;
+  bool has_act = false, has_guard = false, is_sum = false, skip = false;
+  int act_kind = 0;
+  std::vector<InputBinding> inputs;
+  std::vector<std::uint32_t> dof_slots;
+  std::vector<double> sum_items;
+  std::uint32_t n_items = 0, sum_arity = 0;
+  std::vector<double> params;  // per input slot
+  std::uint32_t flags = 0;
+  BlockMap bm;
+  Compiled* k[V_COUNT] = {};
+  // runtime
+  unsigned char* d_mask = nullptr;  // activation mask (all elements)
+  int* d_active = nullptr;          // active list (nullptr = identity)
+  long long n_active = 0;
+  bool act_init = false;
+  int* d_slots = nullptr;
+  double* d_contrib = nullptr;
+  long long contrib_cap = 0;
+  double* d_elemE = nullptr;
+  long long elemE_cap = 0;
+  double* d_values = nullptr;  // activation / guard values per element
+};
+
+}  // namespace
+
+struct symel_cuda_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::string cache_dir;
+  std::vector<Array> arrays;
+  std::vector<Conn> conns;
+  std::vector<std::unique_ptr<Energy>> energies;
+  std::map<std::uint64_t, std::unique_ptr<Compiled>> kcache;
+  // dof layout + pattern
+  bool topology_dirty = true, pattern_dirty = true;
+  int b = 1;
+  long long n_dofs = 0, n_rows = 0, n_blocks = 0;
+  std::vector<long long> set_off;  // per array (-1 if not a dof array)
+  int* d_row_ptr = nullptr;
+  int* d_col_idx = nullptr;
+  double* d_vals = nullptr;
+  double* d_grad = nullptr;
+  unsigned char* d_pins = nullptr;
+  bool any_pins = false;
+  dev::OrderedRefs refs;
+  bool refs_valid = false;
+  // scratch
+  double* d_partial = nullptr;
+  long long partial_cap = 0;
+  double* d_energy = nullptr;  // [n_energies + 1]
+  int* d_bad = nullptr;        // [n_energies]
+  double* h_pinned = nullptr;  // E + bad staging
+  cudaEvent_t ev[4] = {};
+  symel_cuda_timings timings{};
+  std::uint64_t launches = 0;
+  double last_E = 0.0;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+void cfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+template <class T>
+void dalloc(T** p, std::size_t n) {
+  cfree(*p);
+  *p = nullptr;
+  CK(cudaMalloc((void**)p, sizeof(T) * (n ? n : 1)));
+}
+
+Energy& energy_of(symel_cuda_ctx* c, int id) {
+  if (id < 0 || id >= (int)c->energies.size()) throw Fail{SYMEL_E_ARG, "invalid energy handle"};
+  return *c->energies[id];
+}
+
+// ------------------------------------------------------------------------------ NVRTC
+
+Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
+  std::string src = emit_kernel(spec);
+  const std::string flags = spec.fast ? "fmad1" : "fmad0";
+  const std::uint64_t key = fnv1a(src + "|" + flags + "|sm_100a|v1");
+  auto it = c->kcache.find(key);
+  if (it != c->kcache.end()) return it->second.get();
+  char hex[32];
+  std::snprintf(hex, sizeof hex, "%016llx", (unsigned long long)key);
+  std::vector<char> cubin;
+  const std::string path = c->cache_dir.empty() ? "" : c->cache_dir + "/" + hex + ".sm100a.cubin";
+  if (!path.empty()) {
+    std::ifstream is(path, std::ios::binary);
+    if (is) cubin.assign(std::istreambuf_iterator<char>(is), {});
+  }
+  if (cubin.empty()) {
+    const auto t0 = std::chrono::steady_clock::now();
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), (spec.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+      throw Fail{SYMEL_E_COMPILE, "nvrtcCreateProgram failed"};
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo",
+                                     spec.fast ? "--fmad=true" : "--fmad=false"};
+    const nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+    if (r != NVRTC_SUCCESS) {
+      std::size_t ls = 0;
+      nvrtcGetProgramLogSize(prog, &ls);
+      std::string log(ls, '\0');
+      nvrtcGetProgramLog(prog, log.data());
+      nvrtcDestroyProgram(&prog);
+      throw Fail{SYMEL_E_COMPILE, "kernel compilation failed (" + std::string(nvrtcGetErrorString(r)) + "):\n" + log};
+    }
+    std::size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    cubin.resize(n);
+    nvrtcGetCUBIN(prog, cubin.data());
+    nvrtcDestroyProgram(&prog);
+    c->timings.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (!path.empty()) {
+      std::error_code ec;
+      std::filesystem::create_directories(c->cache_dir, ec);
+      const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid());
+      std::ofstream os(tmp, std::ios::binary | std::ios::trunc);
+      os.write(cubin.data(), (std::streamsize)cubin.size());
+      os.close();
+      std::filesystem::rename(tmp, path, ec);
+    }
+  }
+  auto comp = std::make_unique<Compiled>();
+  comp->source = std::move(src);
+  comp->tpb = spec.threads_per_block;
+  if (c->device >= 0) {
+    CK(cudaLibraryLoadData(&comp->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    CK(cudaLibraryGetKernel(&comp->kernel, comp->lib, spec.name.c_str()));
+  }
+  Compiled* raw = comp.get();
+  c->kcache.emplace(key, std::move(comp));
+  return raw;
+}
+
+KernelSpec base_spec(symel_cuda_ctx* c, const Energy& e, const TapeIR* tape) {
+  KernelSpec s;
+  s.tape = tape;
+  s.inputs = e.inputs;
+  s.dof_slots = e.dof_slots;
+  for (const Array& a : c->arrays) s.array_comps.push_back(a.comps);
+  s.arity = c->conns[e.conn].arity;
+  s.sum_items = e.sum_items;
+  s.n_items = e.n_items;
+  s.sum_arity = e.sum_arity;
+  s.b = c->b;
+  return s;
+}
+
+Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
+  if (e.k[v]) return e.k[v];
+  KernelSpec s;
+  switch (v) {
+    case V_CONTRIB_IEEE:
+      s = base_spec(c, e, &e.deriv);
+      s.mode = OutMode::contrib;
+      s.fast = false;
+      s.schedule = 0;  // tape order: bitwise the reference's sequence of operations
+      break;
+    case V_CONTRIB_FAST:
+      s = base_spec(c, e, &e.deriv);
+      s.mode = OutMode::contrib;
+      break;
+    case V_ATOMIC:
+      s = base_spec(c, e, &e.deriv);
+      s.mode = OutMode::fused_atomic;
+      break;
+    case V_ENERGY:
+      s = base_spec(c, e, &e.eonly);
+      s.mode = OutMode::value_only;
+      s.value_reduce = 3;
+      s.threads_per_block = 256;
+      break;
+    case V_ACT:
+      s = base_spec(c, e, &e.act);
+      s.mode = OutMode::value_only;
+      s.value_reduce = 1;
+      s.threads_per_block = 256;
+      break;
+    case V_GUARD:
+      s = base_spec(c, e, &e.guard);
+      s.mode = OutMode::value_only;
+      s.value_reduce = 2;
+      s.threads_per_block = 256;
+      break;
+    default:
+      throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
+  }
+  s.name = "sy_" + std::to_string(v);
+  e.k[v] = compile_kernel(c, s);
+  return e.k[v];
+}
+
+void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n) {
+  if (n <= 0) return;
+  if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+  const long long blocks = (n - a.t0 + k->tpb - 1) / k->tpb;
+  void* params[] = {&a};
+  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, 0, c->stream));
+  ++c->launches;
+}
+
+void fill_args(symel_cuda_ctx* c, const Energy& e, SyArgs& a) {
+  std::memset(&a, 0, sizeof a);
+  if (c->arrays.size() > 24) throw Fail{SYMEL_E_ARG, "too many arrays (max 24)"};
+  for (std::size_t i = 0; i < c->arrays.size(); ++i) {
+    a.arr[i] = c->arrays[i].d;
+    a.set_off[i] = i < c->set_off.size() ? c->set_off[i] : -1;
+  }
+  a.conn = c->conns[e.conn].d;
+  int np = 0;
+  for (std::size_t k = 0; k < e.inputs.size(); ++k)
+    if (e.inputs[k].kind == InKind::param) a.params[np++] = e.params[k];
+}
+
+// ------------------------------------------------------------------------ layout/pattern
+
+void refresh_layout(symel_cuda_ctx* c) {
+  c->set_off.assign(c->arrays.size(), -1);
+  long long off = 0;
+  bool all3 = true, any = false;
+  for (std::size_t i = 0; i < c->arrays.size(); ++i) {
+    const Array& a = c->arrays[i];
+    if (!a.is_dof) continue;
+    any = true;
+    c->set_off[i] = off;
+    off += (long long)a.items * a.comps;
+    if (a.comps != 3) all3 = false;
+  }
+  const int nb = (any && all3) ? 3 : 1;  // assembly.hpp:273-276
+  if (nb != c->b) {
+    c->b = nb;
+    for (auto& e : c->energies)
+      for (auto& k : e->k) k = nullptr;  // kernels are specialised on b
+  }
+  c->n_dofs = off;
+  c->n_rows = off / c->b;
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    KernelSpec s = base_spec(c, e, &e.deriv);
+    e.bm = make_block_map(s);
+    if (e.bm.n_lb > (unsigned)dev::kMaxLb) throw Fail{SYMEL_E_ARG, "energy '" + e.name + "': too many local blocks"};
+  }
+}
+
+dev::LbDesc lb_desc(symel_cuda_ctx* c, const Energy& e) {
+  dev::LbDesc d{};
+  d.n_lb = (int)e.bm.n_lb;
+  d.b = c->b;
+  d.arity = (int)c->conns[e.conn].arity;
+  for (std::uint32_t q = 0; q < e.bm.n_lb; ++q) {
+    d.slot[q] = (int)e.bm.lb_slot[q];
+    d.off[q] = c->set_off[e.bm.lb_array[q]] + e.bm.lb_comp0[q];
+    d.comps[q] = (int)c->arrays[e.bm.lb_array[q]].comps;
+  }
+  return d;
+}
+
+void build_pattern(symel_cuda_ctx* c) {
+  cudaEventRecord(c->ev[0], c->stream);
+  cfree(c->d_row_ptr); c->d_row_ptr = nullptr;
+  cfree(c->d_col_idx); c->d_col_idx = nullptr;
+  long long cap = c->n_rows;
+  for (auto& ep : c->energies)
+    if (!ep->skip) cap += ep->n_active * (long long)ep->bm.n_lb * (ep->bm.n_lb - 1);
+  unsigned long long* keys = nullptr;
+  unsigned long long* counter = nullptr;
+  CK(cudaMallocAsync((void**)&keys, sizeof(unsigned long long) * (cap ? cap : 1), c->stream));
+  CK(cudaMallocAsync((void**)&counter, sizeof(unsigned long long), c->stream));
+  const unsigned long long init = (unsigned long long)c->n_rows;
+  CK(cudaMemcpyAsync(counter, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+  CK(dev::diag_keys(c->n_rows, keys, c->stream));
+  ++c->launches;
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    if (e.skip || e.n_active == 0) continue;
+    CK(dev::pattern_keys(lb_desc(c, e), c->conns[e.conn].d, e.d_active, e.n_active, keys, counter, c->stream));
+    ++c->launches;
+  }
+  unsigned long long nk = 0;
+  CK(cudaMemcpyAsync(&nk, counter, sizeof nk, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  long long nb = 0;
+  CK(dev::build_csr(keys, (long long)nk, c->n_rows, &c->d_row_ptr, &c->d_col_idx, &nb, c->stream));
+  c->n_blocks = nb;
+  CK(cudaFreeAsync(keys, c->stream));
+  CK(cudaFreeAsync(counter, c->stream));
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    cfree(e.d_slots); e.d_slots = nullptr;
+    if (e.skip || e.n_active == 0) continue;
+    dalloc(&e.d_slots, (std::size_t)e.n_active * e.bm.n_lb * e.bm.n_lb);
+    CK(dev::slot_map(lb_desc(c, e), c->conns[e.conn].d, e.d_active, e.n_active, c->d_row_ptr, c->d_col_idx,
+                     e.d_slots, c->stream));
+    ++c->launches;
+  }
+  dalloc(&c->d_vals, (std::size_t)c->n_blocks * c->b * c->b);
+  dalloc(&c->d_grad, (std::size_t)c->n_dofs);
+  CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
+  CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
+  if (c->refs_valid) dev::free_ordered_refs(&c->refs);
+  c->refs_valid = false;
+  c->pattern_dirty = false;
+  cudaEventRecord(c->ev[1], c->stream);
+  cudaEventSynchronize(c->ev[1]);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+  c->timings.pattern_ms = ms;
+}
+
+void ensure_refs(symel_cuda_ctx* c) {
+  if (c->refs_valid) return;
+  std::vector<dev::EnergyRefSrc> src;
+  long long ord = 0;
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    if (e.skip) continue;
+    dev::EnergyRefSrc r{};
+    r.slots = e.d_slots;
+    r.conn = c->conns[e.conn].d;
+    r.active = e.d_active;
+    r.n_active = e.n_active;
+    r.ord_base = ord;
+    r.d = lb_desc(c, e);
+    ord += e.n_active;
+    src.push_back(r);
+  }
+  CK(dev::ordered_refs(src.data(), (int)src.size(), c->n_blocks, c->n_rows, &c->refs, c->stream));
+  c->launches += 2 * src.size() + 4;
+  c->refs_valid = true;
+}
+
+// ------------------------------------------------------------------------ activation
+
+void refresh_activation(symel_cuda_ctx* c) {
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    const long long ne = (long long)c->conns[e.conn].n;
+    if (e.skip) { e.n_active = 0; continue; }
+    if (!e.has_act) {
+      if (e.n_active != ne || e.d_active) {
+        cfree(e.d_active); e.d_active = nullptr;
+        e.n_active = ne;
+        c->pattern_dirty = true;
+      }
+      continue;
+    }
+    if (!e.act_init) {
+      dalloc(&e.d_mask, (std::size_t)ne);
+      CK(cudaMemsetAsync(e.d_mask, 1, (std::size_t)(ne ? ne : 1), c->stream));  // prepare(): all active
+      dalloc(&e.d_values, (std::size_t)ne);
+      e.act_init = true;
+      e.n_active = -1;
+    }
+    Compiled* k = kernel_for(c, e, V_ACT);
+    SyArgs a;
+    fill_args(c, e, a);
+    a.n = ne;
+    a.value_out = e.d_values;
+    launch(c, k, a, ne);
+    int* d_changed = nullptr;
+    CK(cudaMallocAsync((void**)&d_changed, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(d_changed, 0, sizeof(int), c->stream));
+    CK(dev::activation_mask(e.d_values, ne, e.act_kind, e.d_mask, d_changed, c->stream));
+    ++c->launches;
+    int changed = 0;
+    CK(cudaMemcpyAsync(&changed, d_changed, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaFreeAsync(d_changed, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (changed || e.n_active < 0) {
+      dalloc(&e.d_active, (std::size_t)ne);
+      long long na = 0;
+      CK(dev::compact_active(e.d_mask, ne, e.d_active, &na, c->stream));
+      ++c->launches;
+      e.n_active = na;
+      c->pattern_dirty = true;
+    }
+  }
+}
+
+void prepare(symel_cuda_ctx* c) {
+  if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device available (the device path has no CPU fallback)"};
+  if (c->energies.empty()) throw Fail{SYMEL_E_STATE, "no energies registered"};
+  if (c->topology_dirty) {
+    refresh_layout(c);
+    for (auto& ep : c->energies) {
+      ep->act_init = false;
+      ep->n_active = -1;
+    }
+    c->topology_dirty = false;
+    c->pattern_dirty = true;
+  }
+}
+
+void ensure_elem_buffers(symel_cuda_ctx* c, Energy& e, bool contrib) {
+  const long long n = std::max<long long>(e.n_active, 1);
+  if (e.elemE_cap < n) {
+    dalloc(&e.d_elemE, (std::size_t)n);
+    e.elemE_cap = n;
+  }
+  if (contrib) {
+    const long long need = n * (long long)e.deriv.n_outputs;
+    if (e.contrib_cap < need) {
+      dalloc(&e.d_contrib, (std::size_t)need);
+      e.contrib_cap = need;
+    }
+  }
+  const long long np = dev::energy_tree_partials(n) + 1;
+  if (c->partial_cap < np) {
+    dalloc(&c->d_partial, (std::size_t)np);
+    c->partial_cap = np;
+  }
+}
+
+int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
+  if (!e.d_active) return t;
+  int v = 0;
+  CK(cudaMemcpy(&v, e.d_active + t, sizeof(int), cudaMemcpyDeviceToHost));
+  (void)c;
+  return v;
+}
+
+double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st) {
+  prepare(c);
+  refresh_activation(c);
+  if (c->pattern_dirty) build_pattern(c);
+  const std::uint32_t mode = flags & 3u;
+  const bool ordered = mode == SYMEL_ASM_ORDERED;
+  const bool atomic = mode == SYMEL_ASM_ATOMIC;
+  const int ne = (int)c->energies.size();
+  if (!c->d_energy) {
+    dalloc(&c->d_energy, 64);
+    dalloc(&c->d_bad, 64);
+    CK(cudaMallocHost((void**)&c->h_pinned, 1024));
+  }
+  if (ne > 60) throw Fail{SYMEL_E_ARG, "too many energies"};
+  std::vector<int> init(ne, INT_MAX);
+  CK(cudaMemcpyAsync(c->d_bad, init.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->d_energy, 0, sizeof(double) * (ne + 1), c->stream));
+  if (!atomic) ensure_refs(c);
+
+  cudaEventRecord(c->ev[0], c->stream);
+  if (atomic) {
+    CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
+    CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
+  }
+  for (int q = 0; q < ne; ++q) {
+    Energy& e = *c->energies[q];
+    if (e.skip || e.n_active == 0) continue;
+    ensure_elem_buffers(c, e, !atomic);
+    Compiled* k = kernel_for(c, e, atomic ? V_ATOMIC : (ordered ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
+    SyArgs a;
+    fill_args(c, e, a);
+    a.active = e.d_active;
+    a.n = e.n_active;
+    a.contrib = e.d_contrib;
+    a.elemE = e.d_elemE;
+    a.grad = c->d_grad;
+    a.vals = c->d_vals;
+    a.slots = e.d_slots;
+    a.bad_elem = c->d_bad + q;
+    launch(c, k, a, e.n_active);
+  }
+  cudaEventRecord(c->ev[1], c->stream);
+  // phase 2: scatter (non-atomic), energy, pins
+  if (!atomic) {
+    std::vector<dev::ContribLayout> lay;
+    long long ord = 0;
+    for (auto& ep : c->energies) {
+      Energy& e = *ep;
+      if (e.skip) continue;
+      dev::ContribLayout L{};
+      L.ord_base = ord;
+      L.ord_end = ord + e.n_active;
+      ord += e.n_active;
+      L.contrib = e.d_contrib;
+      L.stride = (int)e.deriv.n_outputs;
+      L.n_dofs = (int)e.dof_slots.size();
+      L.n_lb = (int)e.bm.n_lb;
+      L.b = c->b;
+      std::memset(L.dof_of, -1, sizeof L.dof_of);
+      for (std::size_t k = 0; k < e.dof_slots.size(); ++k)
+        L.dof_of[e.bm.lb_of_dof[k] * 3 + e.bm.entry_of_dof[k]] = (signed char)k;
+      lay.push_back(L);
+    }
+    if (lay.size() > 8) throw Fail{SYMEL_E_ARG, "ordered scatter supports up to 8 energies"};
+    CK(dev::ordered_scatter(lay.data(), (int)lay.size(), c->refs, c->n_blocks, c->n_rows, c->d_vals, c->d_grad,
+                            c->stream));
+    c->launches += 2;
+  }
+  if (ordered) {
+    std::vector<const double*> ptrs;
+    std::vector<long long> strides, counts;
+    for (auto& ep : c->energies) {
+      if (ep->skip || ep->n_active == 0) continue;
+      ptrs.push_back(ep->d_contrib);
+      strides.push_back(ep->deriv.n_outputs);
+      counts.push_back(ep->n_active);
+    }
+    CK(dev::energy_serial(ptrs.data(), strides.data(), counts.data(), (int)ptrs.size(), c->d_energy + ne, c->stream));
+    c->launches += 2 * ptrs.size();
+  } else {
+    for (int q = 0; q < ne; ++q) {
+      Energy& e = *c->energies[q];
+      if (e.skip || e.n_active == 0) continue;
+      const double* v = atomic ? e.d_elemE : e.d_contrib;
+      const long long stride = atomic ? 1 : e.deriv.n_outputs;
+      CK(dev::energy_tree(v, stride, e.n_active, c->d_partial, c->d_energy + q, c->stream));
+      c->launches += 2;
+    }
+    CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
+    ++c->launches;
+  }
+  if (c->any_pins) {
+    CK(dev::apply_pins(c->d_pins, c->n_rows, c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->d_grad, c->stream));
+    ++c->launches;
+  }
+  cudaEventRecord(c->ev[2], c->stream);
+  CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * ne, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  float m1 = 0, m2 = 0;
+  cudaEventElapsedTime(&m1, c->ev[0], c->ev[1]);
+  cudaEventElapsedTime(&m2, c->ev[1], c->ev[2]);
+  c->timings.eval_ms = m1;
+  c->timings.assemble_ms = m2;
+  const double E = c->h_pinned[0];
+  const int* bad = reinterpret_cast<const int*>(c->h_pinned + 1);
+  if (st) *st = symel_cuda_status{SYMEL_OK, -1, -1};
+  for (int q = 0; q < ne; ++q) {
+    if (bad[q] != INT_MAX) {
+      const Energy& e = *c->energies[q];
+      const int64_t el = element_of(c, e, bad[q]);
+      if (st) *st = symel_cuda_status{SYMEL_E_NONFINITE, q, el};
+      throw Fail{SYMEL_E_NONFINITE, "energy '" + e.name + "': non-finite derivative output at element " + std::to_string(el)};
+    }
+  }
+  c->last_E = E;
+  return E;
+}
+
+template <class F>
+int guarded(symel_cuda_ctx* c, F&& f) {
+  if (!c) return SYMEL_E_ARG;
+  try {
+    f();
+    return SYMEL_OK;
+  } catch (const Fail& e) {
+    c->err = e.msg;
+    return e.code;
+  } catch (const TapeError& e) {
+    c->err = e.what();
+    return SYMEL_E_TAPE;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return SYMEL_E_ARG;
+  }
+}
+
+TapeIR energy_only_tape(const TapeIR& d) {
+  TapeIR t = d;
+  t.out_regs = {d.out_regs.at(0)};
+  t.n_outputs = 1;
+  return t;
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+
+extern "C" {
+
+int symel_cuda_abi_version(void) { return SYMEL_CUDA_ABI_VERSION; }
+
+int symel_cuda_create(int device, symel_cuda_ctx** out) {
+  if (!out) return SYMEL_E_ARG;
+  *out = nullptr;
+  auto c = std::make_unique<symel_cuda_ctx>();
+  int n = 0;
+  if (device < 0) {
+    c->device = -1;  // codegen-only context: NVRTC compile + cache, no launches
+  } else if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    g_create_error = "no CUDA device available (the device path has no CPU fallback)";
+    return SYMEL_E_NODEVICE;
+  } else {
+    if (device >= n) return SYMEL_E_ARG;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) return SYMEL_E_CUDA;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return SYMEL_E_CUDA;
+    for (auto& ev : c->ev) cudaEventCreate(&ev);
+  }
+  if (const char* d = std::getenv("SYMEL_CUDA_CACHE")) c->cache_dir = d;
+  *out = c.release();
+  return SYMEL_OK;
+}
+
+void symel_cuda_destroy(symel_cuda_ctx* c) {
+  if (!c) return;
+  if (c->device >= 0) {
+    cudaStreamSynchronize(c->stream);
+    for (Array& a : c->arrays) cfree(a.d);
+    for (Conn& k : c->conns) cfree(k.d);
+    for (auto& e : c->energies) {
+      cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
+      cfree(e->d_values);
+    }
+    cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
+    cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
+    if (c->refs_valid) dev::free_ordered_refs(&c->refs);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    for (auto& kv : c->kcache)
+      if (kv.second->lib) cudaLibraryUnload(kv.second->lib);
+    for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
+    cudaStreamDestroy(c->stream);
+  }
+  delete c;
+}
+
+const char* symel_cuda_last_error(const symel_cuda_ctx* c) {
+  return c ? c->err.c_str() : g_create_error.c_str();
+}
+
+int symel_cuda_set_cache_dir(symel_cuda_ctx* c, const char* dir) {
+  return guarded(c, [&] { c->cache_dir = dir ? dir : ""; });
+}
+
+int symel_cuda_add_array(symel_cuda_ctx* c, const char* name, uint64_t items, uint32_t comps, int is_dof, int* id) {
+  return guarded(c, [&] {
+    if (comps == 0) throw Fail{SYMEL_E_ARG, std::string("array '") + (name ? name : "") + "': component count must be positive"};
+    for (const Array& a : c->arrays)
+      if (a.name == name) throw Fail{SYMEL_E_ARG, "array '" + a.name + "' already registered"};
+    if (c->arrays.size() >= 24) throw Fail{SYMEL_E_ARG, "too many arrays (max 24)"};
+    Array a;
+    a.name = name ? name : "";
+    a.items = items;
+    a.comps = comps;
+    a.is_dof = is_dof != 0;
+    if (c->device >= 0) {
+      dalloc(&a.d, (std::size_t)(items * comps));
+      CK(cudaMemset(a.d, 0, sizeof(double) * items * comps));
+    }
+    c->arrays.push_back(a);
+    c->topology_dirty = true;
+    if (id) *id = (int)c->arrays.size() - 1;
+  });
+}
+
+static Array& array_of(symel_cuda_ctx* c, int id) {
+  if (id < 0 || id >= (int)c->arrays.size()) throw Fail{SYMEL_E_ARG, "invalid array handle"};
+  return c->arrays[id];
+}
+
+int symel_cuda_set_array(symel_cuda_ctx* c, int id, const double* host, uint64_t count) {
+  return guarded(c, [&] {
+    Array& a = array_of(c, id);
+    if (count != a.items * a.comps) throw Fail{SYMEL_E_ARG, "array '" + a.name + "': size mismatch"};
+    if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+    CK(cudaMemcpyAsync(a.d, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_get_array(symel_cuda_ctx* c, int id, double* host, uint64_t count) {
+  return guarded(c, [&] {
+    Array& a = array_of(c, id);
+    if (count != a.items * a.comps) throw Fail{SYMEL_E_ARG, "array '" + a.name + "': size mismatch"};
+    if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+    CK(cudaMemcpyAsync(host, a.d, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_array_device_ptr(symel_cuda_ctx* c, int id, double** p) {
+  return guarded(c, [&] { *p = array_of(c, id).d; });
+}
+
+int symel_cuda_add_connectivity(symel_cuda_ctx* c, const char* name, uint32_t arity, int* id) {
+  return guarded(c, [&] {
+    if (arity == 0) throw Fail{SYMEL_E_ARG, std::string("connectivity '") + (name ? name : "") + "': arity must be positive"};
+    Conn k;
+    k.name = name ? name : "";
+    k.arity = arity;
+    c->conns.push_back(k);
+    c->topology_dirty = true;
+    if (id) *id = (int)c->conns.size() - 1;
+  });
+}
+
+int symel_cuda_set_elements(symel_cuda_ctx* c, int id, const int64_t* flat, uint64_t n_elems) {
+  return guarded(c, [&] {
+    if (id < 0 || id >= (int)c->conns.size()) throw Fail{SYMEL_E_ARG, "invalid connectivity handle"};
+    Conn& k = c->conns[id];
+    std::vector<int> v((std::size_t)(n_elems * k.arity));
+    for (std::size_t i = 0; i < v.size(); ++i) {
+      if (flat[i] < 0 || flat[i] > INT_MAX)
+        throw Fail{SYMEL_E_ARG, "connectivity '" + k.name + "': element " + std::to_string(i / k.arity) +
+                                    " references item " + std::to_string(flat[i]) + " outside the int32 range"};
+      v[i] = (int)flat[i];
+    }
+    k.n = n_elems;
+    if (c->device >= 0) {
+      dalloc(&k.d, v.size());
+      CK(cudaMemcpy(k.d, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
+    }
+    c->topology_dirty = true;
+  });
+}
+
+int symel_cuda_add_energy(symel_cuda_ctx* c, const char* name, int conn_id, const uint8_t* deriv_tape, uint64_t deriv_len,
+                          const symel_input_src* inputs, uint32_t n_inputs, const uint32_t* dof_slots, uint32_t n_dofs,
+                          const double* sum_items, uint32_t n_items, uint32_t sum_arity, const uint8_t* act_tape,
+                          uint64_t act_len, int act_kind, const uint8_t* guard_tape, uint64_t guard_len, int* id) {
+  return guarded(c, [&] {
+    auto e = std::make_unique<Energy>();
+    e->name = name ? name : "";
+    for (auto& d : c->energies)
+      if (d->name == e->name) throw Fail{SYMEL_E_ARG, "energy '" + e->name + "' already registered"};
+    if (conn_id < 0 || conn_id >= (int)c->conns.size()) throw Fail{SYMEL_E_ARG, "invalid connectivity handle"};
+    e->conn = conn_id;
+    e->deriv = parse_tape(deriv_tape, deriv_len);
+    if (e->deriv.n_inputs != n_inputs) throw Fail{SYMEL_E_ARG, "energy '" + e->name + "': tape input count mismatch"};
+    if (e->deriv.n_dofs != n_dofs || e->deriv.n_outputs != 1 + n_dofs + n_dofs * n_dofs)
+      throw Fail{SYMEL_E_ARG, "energy '" + e->name + "': cached kernel layout mismatch"};
+    const std::uint32_t arity = c->conns[conn_id].arity;
+    for (uint32_t k = 0; k < n_inputs; ++k) {
+      InputBinding b;
+      b.kind = static_cast<InKind>(inputs[k].kind);
+      b.array = inputs[k].array;
+      b.tuple_slot = inputs[k].tuple_slot;
+      b.comp = inputs[k].comp;
+      if (inputs[k].kind > 3) throw Fail{SYMEL_E_ARG, "invalid input kind"};
+      if ((b.kind == InKind::item_comp || b.kind == InKind::elem_comp) &&
+          (b.array >= c->arrays.size() || b.comp >= c->arrays[b.array].comps))
+        throw Fail{SYMEL_E_ARG, "energy '" + e->name + "': input " + std::to_string(k) + " binds an invalid array/comp"};
+      if (b.kind == InKind::item_comp && b.tuple_slot >= arity)
+        throw Fail{SYMEL_E_ARG, "energy '" + e->name + "': tuple slot " + std::to_string(b.tuple_slot) +
+                                    " outside connectivity arity " + std::to_string(arity)};
+      if (b.kind == InKind::sum_comp && b.tuple_slot >= sum_arity)
+        throw Fail{SYMEL_E_ARG, "energy '" + e->name + "': sum item column out of range"};
+      e->inputs.push_back(b);
+    }
+    e->dof_slots.assign(dof_slots, dof_slots + n_dofs);
+    for (auto s : e->dof_slots) {
+      if (s >= n_inputs || e->inputs[s].kind != InKind::item_comp || !c->arrays[e->inputs[s].array].is_dof)
+        throw Fail{SYMEL_E_ARG, "energy '" + e->name + "': dof slot does not bind a dof array item"};
+    }
+    e->is_sum = sum_arity > 0;
+    e->n_items = e->is_sum ? n_items : 0;
+    e->sum_arity = sum_arity;
+    if (e->is_sum && n_items) e->sum_items.assign(sum_items, sum_items + (std::size_t)n_items * sum_arity);
+    e->skip = e->is_sum && n_items == 0;
+    e->params.assign(n_inputs, 0.0);
+    if (act_tape) {
+      e->act = parse_tape(act_tape, act_len);
+      e->has_act = true;
+      e->act_kind = act_kind;
+      if (e->act.n_outputs != 1) throw Fail{SYMEL_E_ARG, "activation tape must have one output"};
+    }
+    if (guard_tape) {
+      e->guard = parse_tape(guard_tape, guard_len);
+      e->has_guard = true;
+      if (e->guard.n_outputs != 1) throw Fail{SYMEL_E_ARG, "guard tape must have one output"};
+    }
+    e->eonly = energy_only_tape(e->deriv);
+    c->energies.push_back(std::move(e));
+    c->topology_dirty = true;
+    if (id) *id = (int)c->energies.size() - 1;
+  });
+}
+
+int symel_cuda_set_param(symel_cuda_ctx* c, int eid, uint32_t slot, double value) {
+  return guarded(c, [&] {
+    Energy& e = energy_of(c, eid);
+    if (slot >= e.inputs.size() || e.inputs[slot].kind != InKind::param)
+      throw Fail{SYMEL_E_ARG, "energy '" + e.name + "': input " + std::to_string(slot) + " is not a param"};
+    e.params[slot] = value;
+  });
+}
+
+int symel_cuda_set_energy_flags(symel_cuda_ctx* c, int eid, uint32_t flags) {
+  return guarded(c, [&] {
+    Energy& e = energy_of(c, eid);
+    if (e.flags != flags) {
+      e.flags = flags;
+      for (auto& k : e.k) k = nullptr;
+    }
+  });
+}
+
+int symel_cuda_set_pins(symel_cuda_ctx* c, const uint8_t* mask, uint64_t n) {
+  return guarded(c, [&] {
+    prepare(c);
+    if ((long long)n != c->n_dofs) throw Fail{SYMEL_E_ARG, "pins: mask size mismatch"};
+    c->any_pins = false;
+    for (uint64_t i = 0; i < n; ++i) c->any_pins = c->any_pins || mask[i];
+    dalloc(&c->d_pins, (std::size_t)n);
+    CK(cudaMemcpy(c->d_pins, mask, n, cudaMemcpyHostToDevice));
+  });
+}
+
+int symel_cuda_assemble(symel_cuda_ctx* c, uint32_t flags, double* energy, symel_cuda_status* st) {
+  if (st) *st = symel_cuda_status{SYMEL_OK, -1, -1};
+  return guarded(c, [&] {
+    const double E = do_assemble(c, flags, st);
+    if (energy) *energy = E;
+  });
+}
+
+int symel_cuda_energy_only(symel_cuda_ctx* c, double* out) {
+  return guarded(c, [&] {
+    prepare(c);
+    if (c->pattern_dirty) {
+      // activation frozen since the last assemble (assembly.hpp:128-139); first call: all
+      refresh_activation(c);
+      build_pattern(c);
+    }
+    const int ne = (int)c->energies.size();
+    if (!c->d_energy) {
+      dalloc(&c->d_energy, 64);
+      dalloc(&c->d_bad, 64);
+      CK(cudaMallocHost((void**)&c->h_pinned, 1024));
+    }
+    CK(cudaMemsetAsync(c->d_energy, 0, sizeof(double) * (ne + 1), c->stream));
+    for (int q = 0; q < ne; ++q) {
+      Energy& e = *c->energies[q];
+      if (e.skip || e.n_active == 0) continue;
+      ensure_elem_buffers(c, e, false);
+      Compiled* k = kernel_for(c, e, V_ENERGY);
+      SyArgs a;
+      fill_args(c, e, a);
+      a.active = e.d_active;
+      a.n = e.n_active;
+      a.value_out = e.d_elemE;
+      launch(c, k, a, e.n_active);
+      CK(dev::energy_tree(e.d_elemE, 1, e.n_active, c->d_partial, c->d_energy + q, c->stream));
+      c->launches += 2;
+    }
+    CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
+    CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = c->h_pinned[0];
+  });
+}
+
+int symel_cuda_guard_min(symel_cuda_ctx* c, double* gmin) {
+  return guarded(c, [&] {
+    prepare(c);
+    double best = std::numeric_limits<double>::infinity();
+    for (auto& ep : c->energies) {
+      Energy& e = *ep;
+      if (!e.has_guard || e.skip) continue;
+      const long long ne = (long long)c->conns[e.conn].n;
+      if (ne == 0) continue;
+      if (!e.d_values) dalloc(&e.d_values, (std::size_t)ne);
+      Compiled* k = kernel_for(c, e, V_GUARD);
+      SyArgs a;
+      fill_args(c, e, a);
+      a.n = ne;
+      a.value_out = e.d_values;
+      launch(c, k, a, ne);
+      double* d_min = nullptr;
+      CK(cudaMallocAsync((void**)&d_min, sizeof(double), c->stream));
+      CK(dev::min_reduce(e.d_values, ne, d_min, c->stream));
+      double v = 0;
+      CK(cudaMemcpyAsync(&v, d_min, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaFreeAsync(d_min, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      best = v < best ? v : best;
+    }
+    *gmin = best;
+  });
+}
+
+int symel_cuda_pattern_info(symel_cuda_ctx* c, int* b, uint64_t* nbr, uint64_t* nb, uint64_t* nd) {
+  return guarded(c, [&] {
+    if (b) *b = c->b;
+    if (nbr) *nbr = (uint64_t)c->n_rows;
+    if (nb) *nb = (uint64_t)c->n_blocks;
+    if (nd) *nd = (uint64_t)c->n_dofs;
+  });
+}
+
+int symel_cuda_copy_pattern(symel_cuda_ctx* c, int64_t* row_ptr, int64_t* col_idx) {
+  return guarded(c, [&] {
+    std::vector<int> rp((std::size_t)c->n_rows + 1), ci((std::size_t)c->n_blocks);
+    CK(cudaMemcpy(rp.data(), c->d_row_ptr, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost));
+    if (!ci.empty()) CK(cudaMemcpy(ci.data(), c->d_col_idx, sizeof(int) * ci.size(), cudaMemcpyDeviceToHost));
+    for (std::size_t i = 0; i < rp.size(); ++i) row_ptr[i] = rp[i];
+    for (std::size_t i = 0; i < ci.size(); ++i) col_idx[i] = ci[i];
+  });
+}
+
+int symel_cuda_copy_gradient(symel_cuda_ctx* c, double* host) {
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(host, c->d_grad, sizeof(double) * c->n_dofs, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_copy_hessian(symel_cuda_ctx* c, double* host) {
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(host, c->d_vals, sizeof(double) * c->n_blocks * c->b * c->b, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_device_results(symel_cuda_ctx* c, const double** g, const double** v, const int32_t** rp,
+                              const int32_t** ci) {
+  return guarded(c, [&] {
+    if (g) *g = c->d_grad;
+    if (v) *v = c->d_vals;
+    if (rp) *rp = c->d_row_ptr;
+    if (ci) *ci = c->d_col_idx;
+  });
+}
+
+int symel_cuda_active_count(symel_cuda_ctx* c, int eid, uint64_t* n) {
+  return guarded(c, [&] { *n = (uint64_t)std::max<long long>(0, energy_of(c, eid).n_active); });
+}
+
+int symel_cuda_copy_active(symel_cuda_ctx* c, int eid, uint8_t* mask) {
+  return guarded(c, [&] {
+    Energy& e = energy_of(c, eid);
+    const std::size_t ne = (std::size_t)c->conns[e.conn].n;
+    if (!e.has_act || !e.d_mask) {
+      std::memset(mask, e.skip ? 0 : 1, ne);
+      return;
+    }
+    CK(cudaMemcpy(mask, e.d_mask, ne, cudaMemcpyDeviceToHost));
+  });
+}
+
+int symel_cuda_element_outputs(symel_cuda_ctx* c, int eid, uint64_t first, uint64_t count, uint32_t flags, double* out) {
+  return guarded(c, [&] {
+    prepare(c);
+    Energy& e = energy_of(c, eid);
+    const std::uint64_t ne = c->conns[e.conn].n;
+    if (first + count > ne) throw Fail{SYMEL_E_ARG, "element range out of bounds"};
+    if (count == 0) return;
+    std::vector<int> ids(count);
+    for (std::uint64_t i = 0; i < count; ++i) ids[i] = (int)(first + i);
+    int* d_ids = nullptr;
+    double* d_out = nullptr;
+    int* d_bad = nullptr;
+    const std::size_t stride = e.deriv.n_outputs;
+    CK(cudaMalloc((void**)&d_ids, sizeof(int) * count));
+    CK(cudaMalloc((void**)&d_out, sizeof(double) * count * stride));
+    CK(cudaMalloc((void**)&d_bad, sizeof(int)));
+    CK(cudaMemcpy(d_ids, ids.data(), sizeof(int) * count, cudaMemcpyHostToDevice));
+    Compiled* k = kernel_for(c, e, (flags & 3u) == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST);
+    SyArgs a;
+    fill_args(c, e, a);
+    a.active = d_ids;
+    a.n = (long long)count;
+    a.contrib = d_out;
+    a.bad_elem = d_bad;
+    launch(c, k, a, (long long)count);
+    CK(cudaMemcpyAsync(out, d_out, sizeof(double) * count * stride, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d_ids); cudaFree(d_out); cudaFree(d_bad);
+  });
+}
+
+int symel_cuda_get_timings(symel_cuda_ctx* c, symel_cuda_timings* t) {
+  return guarded(c, [&] { *t = c->timings; });
+}
+
+int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* buf, uint64_t len, uint64_t* needed) {
+  return guarded(c, [&] {
+    Energy& e = energy_of(c, eid);
+    if (c->topology_dirty) refresh_layout(c);
+    const std::uint32_t mode = flags & 3u;
+    KernelSpec s = base_spec(c, e, &e.deriv);
+    s.mode = mode == SYMEL_ASM_ATOMIC ? OutMode::fused_atomic : OutMode::contrib;
+    s.fast = mode != SYMEL_ASM_ORDERED;
+    s.schedule = mode == SYMEL_ASM_ORDERED ? 0 : 1;
+    const std::string src = emit_kernel(s);
+    if (needed) *needed = src.size() + 1;
+    if (buf && len) {
+      const std::size_t n = std::min<std::size_t>(len - 1, src.size());
+      std::memcpy(buf, src.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+int symel_cuda_launch_count(symel_cuda_ctx* c, uint64_t* n) {
+  return guarded(c, [&] { *n = c->launches; });
+}
+
+int symel_cuda_precompile(symel_cuda_ctx* c, int eid, uint32_t flags) {
+  return guarded(c, [&] {
+    Energy& e = energy_of(c, eid);
+    if (c->topology_dirty) refresh_layout(c);
+    const std::uint32_t mode = flags & 3u;
+    kernel_for(c, e, mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : (mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
+    if (mode != SYMEL_ASM_ORDERED) kernel_for(c, e, V_ENERGY);
+    if (e.has_act) kernel_for(c, e, V_ACT);
+    if (e.has_guard) kernel_for(c, e, V_GUARD);
+  });
+}
+
+int symel_cuda_fp64_peak(symel_cuda_ctx* c, double* tflops) {
+  return guarded(c, [&] {
+    if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    CK(dev::fp64_peak(nsm, tflops, c->stream));
+    ++c->launches;
+  });
+}
+
+int symel_cuda_sync(symel_cuda_ctx* c) {
+  return guarded(c, [&] {
+    if (c->device >= 0) CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_stream(symel_cuda_ctx* c, void** s) {
+  return guarded(c, [&] { *s = (void*)c->stream; });
+}
+
+}  // extern "C"

@@ -53,7 +53,9 @@ typedef struct {
 /* Activation comparison = symel::CmpKind (expr.hpp:569): 0 = ge (v >= 0), 1 = gt (v > 0). */
 
 /* Energy flags (symel_cuda_set_energy_flags). */
-#define SYMEL_ENERGY_SPD 0x1u /* project each element Hessian to SPD (clamp eigenvalues < 0) */
+#define SYMEL_ENERGY_SPD 0x1u   /* project each element Hessian to SPD (clamp eigenvalues < 0) */
+#define SYMEL_ENERGY_EXACT 0x2u /* evaluate in the reference's rounding (tape order, IEEE division,
+                                   no FMA) in every mode; for ill-conditioned energies */
 
 /* assemble() flags: exactly one assembly mode. */
 #define SYMEL_ASM_DETERMINISTIC 0x0u /* fast eval + tile-ordered atomic-free reduction (default) */

@@ -168,6 +168,14 @@ void dalloc(T** p, std::size_t n) {
   CK(cudaMalloc((void**)p, sizeof(T) * (n ? n : 1)));
 }
 
+// All host<->device traffic is ordered on the context stream (a non-blocking stream does not
+// synchronise with legacy-stream cudaMemcpy/cudaMemset).
+void copy_sync(symel_cuda_ctx* c, void* dst, const void* src, std::size_t bytes, cudaMemcpyKind kind) {
+  if (bytes == 0) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, kind, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
 Energy& energy_of(symel_cuda_ctx* c, int id) {
   if (id < 0 || id >= (int)c->energies.size()) throw Fail{SYMEL_E_ARG, "invalid energy handle"};
   return *c->energies[id];
@@ -276,15 +284,25 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.mode = OutMode::value_only;
       s.value_reduce = 1;
       s.threads_per_block = 256;
+      s.fast = false;  // activation decides the active set: reproduce the reference exactly
+      s.schedule = 0;
       break;
     case V_GUARD:
       s = base_spec(c, e, &e.guard);
       s.mode = OutMode::value_only;
       s.value_reduce = 2;
       s.threads_per_block = 256;
+      s.fast = false;  // line-search guard value: exact
+      s.schedule = 0;
       break;
     default:
       throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
+  }
+  if (e.flags & SYMEL_ENERGY_EXACT) {
+    // ill-conditioned energies: reproduce the reference's rounding (tape order, IEEE division,
+    // no contraction) in every assembly mode
+    s.fast = false;
+    s.schedule = 0;
   }
   s.name = "sy_" + std::to_string(v);
   e.k[v] = compile_kernel(c, s);
@@ -515,7 +533,7 @@ void ensure_elem_buffers(symel_cuda_ctx* c, Energy& e, bool contrib) {
 int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
   if (!e.d_active) return t;
   int v = 0;
-  CK(cudaMemcpy(&v, e.d_active + t, sizeof(int), cudaMemcpyDeviceToHost));
+  copy_sync(c, &v, e.d_active + t, sizeof(int), cudaMemcpyDeviceToHost);
   (void)c;
   return v;
 }
@@ -738,7 +756,7 @@ int symel_cuda_add_array(symel_cuda_ctx* c, const char* name, uint64_t items, ui
     a.is_dof = is_dof != 0;
     if (c->device >= 0) {
       dalloc(&a.d, (std::size_t)(items * comps));
-      CK(cudaMemset(a.d, 0, sizeof(double) * items * comps));
+      CK(cudaMemsetAsync(a.d, 0, sizeof(double) * items * comps, c->stream));
     }
     c->arrays.push_back(a);
     c->topology_dirty = true;
@@ -801,7 +819,7 @@ int symel_cuda_set_elements(symel_cuda_ctx* c, int id, const int64_t* flat, uint
     k.n = n_elems;
     if (c->device >= 0) {
       dalloc(&k.d, v.size());
-      CK(cudaMemcpy(k.d, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice));
+      copy_sync(c, k.d, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice);
     }
     c->topology_dirty = true;
   });
@@ -895,7 +913,7 @@ int symel_cuda_set_pins(symel_cuda_ctx* c, const uint8_t* mask, uint64_t n) {
     c->any_pins = false;
     for (uint64_t i = 0; i < n; ++i) c->any_pins = c->any_pins || mask[i];
     dalloc(&c->d_pins, (std::size_t)n);
-    CK(cudaMemcpy(c->d_pins, mask, n, cudaMemcpyHostToDevice));
+    copy_sync(c, c->d_pins, mask, n, cudaMemcpyHostToDevice);
   });
 }
 
@@ -984,8 +1002,8 @@ int symel_cuda_pattern_info(symel_cuda_ctx* c, int* b, uint64_t* nbr, uint64_t* 
 int symel_cuda_copy_pattern(symel_cuda_ctx* c, int64_t* row_ptr, int64_t* col_idx) {
   return guarded(c, [&] {
     std::vector<int> rp((std::size_t)c->n_rows + 1), ci((std::size_t)c->n_blocks);
-    CK(cudaMemcpy(rp.data(), c->d_row_ptr, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost));
-    if (!ci.empty()) CK(cudaMemcpy(ci.data(), c->d_col_idx, sizeof(int) * ci.size(), cudaMemcpyDeviceToHost));
+    copy_sync(c, rp.data(), c->d_row_ptr, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost);
+    copy_sync(c, ci.data(), c->d_col_idx, sizeof(int) * ci.size(), cudaMemcpyDeviceToHost);
     for (std::size_t i = 0; i < rp.size(); ++i) row_ptr[i] = rp[i];
     for (std::size_t i = 0; i < ci.size(); ++i) col_idx[i] = ci[i];
   });
@@ -1027,7 +1045,7 @@ int symel_cuda_copy_active(symel_cuda_ctx* c, int eid, uint8_t* mask) {
       std::memset(mask, e.skip ? 0 : 1, ne);
       return;
     }
-    CK(cudaMemcpy(mask, e.d_mask, ne, cudaMemcpyDeviceToHost));
+    copy_sync(c, mask, e.d_mask, ne, cudaMemcpyDeviceToHost);
   });
 }
 
@@ -1047,7 +1065,7 @@ int symel_cuda_element_outputs(symel_cuda_ctx* c, int eid, uint64_t first, uint6
     CK(cudaMalloc((void**)&d_ids, sizeof(int) * count));
     CK(cudaMalloc((void**)&d_out, sizeof(double) * count * stride));
     CK(cudaMalloc((void**)&d_bad, sizeof(int)));
-    CK(cudaMemcpy(d_ids, ids.data(), sizeof(int) * count, cudaMemcpyHostToDevice));
+    copy_sync(c, d_ids, ids.data(), sizeof(int) * count, cudaMemcpyHostToDevice);
     Compiled* k = kernel_for(c, e, (flags & 3u) == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST);
     SyArgs a;
     fill_args(c, e, a);

@@ -26,6 +26,7 @@ OK, E_ARG, E_CUDA, E_COMPILE, E_NONFINITE, E_STATE, E_TAPE, E_NODEVICE = range(8
 IN_ITEM, IN_ELEM, IN_PARAM, IN_SUM = range(4)
 ASM_DETERMINISTIC, ASM_ATOMIC, ASM_ORDERED = 0, 1, 2
 ENERGY_SPD = 1
+ENERGY_EXACT = 2
 
 MODES = {"deterministic": ASM_DETERMINISTIC, "atomic": ASM_ATOMIC, "ordered": ASM_ORDERED}
 

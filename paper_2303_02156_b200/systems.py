@@ -20,7 +20,7 @@ from typing import Callable, Dict, Optional
 import numpy as np
 
 from . import configs
-from .device import (DeviceAssembler, ENERGY_SPD, IN_ELEM, IN_ITEM, IN_PARAM, IN_SUM)
+from .device import (DeviceAssembler, ENERGY_EXACT, ENERGY_SPD, IN_ELEM, IN_ITEM, IN_PARAM, IN_SUM)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -152,7 +152,7 @@ class DeviceSystem:
             self.energies["contact"] = A.add_energy(
                 "contact", pc, tapes("contact"), contact_inputs(self.x, off), range(12),
                 act_tape=tapes("contact_act"), act_kind=0, guard_tape=tapes("contact_guard"),
-                params={24: p["kappa"], 25: p["dhat"]}, flags=flags)
+                params={24: p["kappa"], 25: p["dhat"]}, flags=flags | ENERGY_EXACT)
 
     def n_elements(self) -> int:
         return sum(self.asm.active_count(e) for e in self.energies.values())

@@ -151,6 +151,14 @@ int symel_cuda_get_timings(symel_cuda_ctx* ctx, symel_cuda_timings* t);
 /* Generated CUDA source of an energy's derivative kernel for a mode (debug / tests). */
 int symel_cuda_kernel_source(symel_cuda_ctx* ctx, int energy_id, uint32_t flags, char* buf,
                              uint64_t buf_len, uint64_t* needed);
+typedef struct {
+  uint64_t tape_ops;  /* operations of the reference tape (the algorithmic count) */
+  uint64_t fast_ops;  /* operations the fast kernels execute (after factorisation) */
+  uint32_t frontier;  /* affine frontier size m of the factorisation, 0 if not factorised */
+  uint32_t n_dofs, n_inputs, n_outputs, n_items, flags;
+} symel_cuda_energy_stats;
+/* Kernel-level facts about one energy (roofline bookkeeping). */
+int symel_cuda_energy_info(symel_cuda_ctx* ctx, int energy_id, symel_cuda_energy_stats* st);
 /* Number of kernels launched on the device by this context since creation. */
 int symel_cuda_launch_count(symel_cuda_ctx* ctx, uint64_t* count);
 /* Compile (NVRTC, sm_100a) the kernels an assemble mode needs into the cubin cache without

@@ -27,7 +27,10 @@
 #include <string>
 #include <vector>
 
+#include <optional>
+
 #include "codegen.hpp"
+#include "factorize.hpp"
 #include "device_ops.hpp"
 #include "sy_args.h"
 #include "tape_io.hpp"
@@ -104,6 +107,10 @@ struct Energy {
   std::uint32_t flags = 0;
   BlockMap bm;
   Compiled* k[V_COUNT] = {};
+  // linear-frontier factorisation of the derivative tape (fast kernels only; factorize.hpp)
+  std::optional<TapeIR> fact;
+  FactorizeInfo fact_info{};
+  bool fact_tried = false;
   // runtime
   unsigned char* d_mask = nullptr;  // activation mask (all elements)
   int* d_active = nullptr;          // active list (nullptr = identity)
@@ -241,6 +248,17 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
   return raw;
 }
 
+// Tape executed by the fast kernels: the factorised one when the energy has a narrowing
+// affine frontier (and is not flagged exact), else the reference tape.
+const TapeIR* fast_tape(Energy& e) {
+  if (!e.fact_tried) {
+    e.fact_tried = true;
+    if (!(e.flags & SYMEL_ENERGY_EXACT) && !std::getenv("SYMEL_NO_FACTORIZE"))
+      e.fact = factorize_linear_frontier(e.deriv, e.dof_slots, &e.fact_info);
+  }
+  return e.fact ? &*e.fact : &e.deriv;
+}
+
 KernelSpec base_spec(symel_cuda_ctx* c, const Energy& e, const TapeIR* tape) {
   KernelSpec s;
   s.tape = tape;
@@ -266,12 +284,14 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.schedule = 0;  // tape order: bitwise the reference's sequence of operations
       break;
     case V_CONTRIB_FAST:
-      s = base_spec(c, e, &e.deriv);
+      s = base_spec(c, e, fast_tape(e));
       s.mode = OutMode::contrib;
+      s.schedule = e.fact ? 2 : 1;
       break;
     case V_ATOMIC:
-      s = base_spec(c, e, &e.deriv);
+      s = base_spec(c, e, fast_tape(e));
       s.mode = OutMode::fused_atomic;
+      s.schedule = e.fact ? 2 : 1;
       break;
     case V_ENERGY:
       s = base_spec(c, e, &e.eonly);
@@ -902,6 +922,8 @@ int symel_cuda_set_energy_flags(symel_cuda_ctx* c, int eid, uint32_t flags) {
     if (e.flags != flags) {
       e.flags = flags;
       for (auto& k : e.k) k = nullptr;
+      e.fact.reset();
+      e.fact_tried = false;
     }
   });
 }
@@ -1089,10 +1111,11 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
     Energy& e = energy_of(c, eid);
     if (c->topology_dirty) refresh_layout(c);
     const std::uint32_t mode = flags & 3u;
-    KernelSpec s = base_spec(c, e, &e.deriv);
+    const bool exact = mode == SYMEL_ASM_ORDERED || (e.flags & SYMEL_ENERGY_EXACT);
+    KernelSpec s = base_spec(c, e, exact ? &e.deriv : fast_tape(e));
     s.mode = mode == SYMEL_ASM_ATOMIC ? OutMode::fused_atomic : OutMode::contrib;
-    s.fast = mode != SYMEL_ASM_ORDERED;
-    s.schedule = mode == SYMEL_ASM_ORDERED ? 0 : 1;
+    s.fast = !exact;
+    s.schedule = exact ? 0 : (e.fact ? 2 : 1);
     const std::string src = emit_kernel(s);
     if (needed) *needed = src.size() + 1;
     if (buf && len) {
@@ -1100,6 +1123,21 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
       std::memcpy(buf, src.data(), n);
       buf[n] = '\0';
     }
+  });
+}
+
+int symel_cuda_energy_info(symel_cuda_ctx* c, int eid, symel_cuda_energy_stats* st) {
+  return guarded(c, [&] {
+    Energy& e = energy_of(c, eid);
+    const TapeIR* ft = fast_tape(e);
+    st->tape_ops = e.deriv.instrs.size();
+    st->fast_ops = ft->instrs.size();
+    st->frontier = e.fact ? e.fact_info.frontier : 0;
+    st->n_dofs = (uint32_t)e.dof_slots.size();
+    st->n_inputs = e.deriv.n_inputs;
+    st->n_outputs = e.deriv.n_outputs;
+    st->n_items = e.n_items;
+    st->flags = e.flags;
   });
 }
 

@@ -62,8 +62,14 @@ EXPORTS = [
     "symel_cuda_device_results", "symel_cuda_active_count", "symel_cuda_copy_active",
     "symel_cuda_element_outputs", "symel_cuda_get_timings", "symel_cuda_kernel_source",
     "symel_cuda_launch_count", "symel_cuda_fp64_peak", "symel_cuda_precompile", "symel_cuda_sync",
-    "symel_cuda_stream",
+    "symel_cuda_stream", "symel_cuda_energy_info",
 ]
+
+
+class EnergyStats(C.Structure):
+    _fields_ = [("tape_ops", C.c_uint64), ("fast_ops", C.c_uint64), ("frontier", C.c_uint32),
+                ("n_dofs", C.c_uint32), ("n_inputs", C.c_uint32), ("n_outputs", C.c_uint32),
+                ("n_items", C.c_uint32), ("flags", C.c_uint32)]
 
 _lib = None
 
@@ -110,6 +116,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "symel_cuda_launch_count": ([P, C.POINTER(U64)], I),
         "symel_cuda_fp64_peak": ([P, C.POINTER(D)], I),
         "symel_cuda_precompile": ([P, I, C.c_uint32], I),
+        "symel_cuda_energy_info": ([P, I, C.POINTER(EnergyStats)], I),
         "symel_cuda_sync": ([P], I),
         "symel_cuda_stream": ([P, C.POINTER(P)], I),
     }
@@ -315,6 +322,11 @@ class DeviceAssembler:
         n = C.c_uint64()
         self._check(self.lib.symel_cuda_launch_count(self.h, C.byref(n)))
         return n.value
+
+    def energy_info(self, eid: int) -> dict:
+        s = EnergyStats()
+        self._check(self.lib.symel_cuda_energy_info(self.h, eid, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in EnergyStats._fields_}
 
     def precompile(self, eid: int, mode: str = "deterministic") -> None:
         self._check(self.lib.symel_cuda_precompile(self.h, eid, MODES[mode]))

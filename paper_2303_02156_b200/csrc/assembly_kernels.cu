@@ -499,4 +499,294 @@ int apply_pins(const unsigned char* mask, long long n_rows, int b, const int* ro
   return (int)cudaGetLastError();
 }
 
+// =================================================================== tile plan (K3)
+
+namespace {
+
+// Hessian: key (global tile << 32 | block), value (element-in-tile << 10 | li << 5 | lj)
+__global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned* vals) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= src.n_active) return;
+  const int nl = src.d.n_lb;
+  const unsigned long long tile = (unsigned long long)(src.tile_base + t / src.tpb);
+  const unsigned tl = (unsigned)(t % src.tpb);
+  for (int i = 0; i < nl; ++i)
+    for (int j = 0; j < nl; ++j) {
+      const long long q = pos + (t * nl + i) * nl + j;
+      keys[q] = (tile << 32) | (unsigned)src.slots[(t * nl + i) * nl + j];
+      vals[q] = (tl << 10) | ((unsigned)i << 5) | (unsigned)j;
+    }
+}
+
+// gradient: key (global tile << 32 | block row), value (element-in-tile << 5 | li)
+__global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned* vals) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= src.n_active) return;
+  const long long e = src.active ? src.active[t] : t;
+  const int* tup = src.conn + e * src.d.arity;
+  const int nl = src.d.n_lb;
+  const unsigned long long tile = (unsigned long long)(src.tile_base + t / src.tpb);
+  const unsigned tl = (unsigned)(t % src.tpb);
+  for (int i = 0; i < nl; ++i) {
+    keys[pos + t * nl + i] = (tile << 32) | (unsigned)lb_block(src.d, tup, i);
+    vals[pos + t * nl + i] = (tl << 5) | (unsigned)i;
+  }
+}
+
+__global__ void k_split_keys(const unsigned long long* __restrict__ ukeys, long long n, int* __restrict__ seg_tile,
+                             int* __restrict__ seg_target) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  seg_tile[i] = (int)(ukeys[i] >> 32);
+  seg_target[i] = (int)(ukeys[i] & 0xffffffffull);
+}
+
+__global__ void k_count_targets(const int* __restrict__ seg_target, long long n, int* __restrict__ count) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(count + seg_target[i], 1);
+}
+
+// over segments sorted by (target, tile): flag boundary segments
+__global__ void k_boundary_flags(const int* __restrict__ sorted_target, long long n, const int* __restrict__ count,
+                                 int* __restrict__ flag) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = count[sorted_target[i]] > 1;
+}
+
+__global__ void k_seg_dst(const int* __restrict__ sorted_target, const int* __restrict__ sorted_seg,
+                          const int* __restrict__ flag, const int* __restrict__ pos, long long n, int* __restrict__ seg_dst) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  seg_dst[sorted_seg[i]] = flag[i] ? -(pos[i] + 1) : sorted_target[i];
+}
+
+__global__ void k_iota(int* v, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int)i;
+}
+
+__global__ void k_is_zero(const int* __restrict__ count, long long n, unsigned char* __restrict__ flag) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = count[i] == 0;
+}
+
+// sorted int keys -> ptr[k] = first index with key >= k, for k in [0, nseg]
+__global__ void k_int_seg_ptr(const int* __restrict__ keys, long long nk, long long nseg, int* __restrict__ ptr) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nk) {
+    const long long r = keys[i];
+    const long long pr = i == 0 ? -1 : (long long)keys[i - 1];
+    for (long long q = pr + 1; q <= r; ++q) ptr[q] = (int)i;
+    if (i == nk - 1)
+      for (long long q = r + 1; q <= nseg; ++q) ptr[q] = (int)nk;
+  }
+  if (nk == 0 && i <= nseg) ptr[i] = 0;
+}
+
+__global__ void k_fixup(const int* __restrict__ pt_ptr, const int* __restrict__ pt_target, long long n_pt, int w,
+                        const double* __restrict__ partials, double* __restrict__ out) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_pt * w) return;
+  const long long p = q / w;
+  const int ent = (int)(q % w);
+  double acc = 0.0;
+  for (int k = pt_ptr[p]; k < pt_ptr[p + 1]; ++k) acc += partials[(long long)k * w + ent];
+  out[(long long)pt_target[p] * w + ent] = acc;
+}
+
+__global__ void k_zero_targets(const int* __restrict__ tg, long long n, int w, double* __restrict__ out) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n * w) out[(long long)tg[q / w] * w + (q % w)] = 0.0;
+}
+
+template <class T>
+int tmp_alloc(T** p, size_t n, void* s) {
+  return (int)cudaMallocAsync((void**)p, sizeof(T) * (n ? n : 1), S(s));
+}
+
+// Sorts (key, val) and segments it; fills the common part of a SegPlan.
+int build_segments(unsigned long long* keys, unsigned* vals, long long n, long long n_tiles, long long n_targets,
+                   SegPlan* sp, void* s) {
+  int err;
+  unsigned long long* k2;
+  unsigned* v2;
+  if ((err = tmp_alloc(&k2, n, s)) || (err = tmp_alloc(&v2, n, s))) return err;
+  const int end_bit = 32 + bits_for((unsigned long long)n_tiles);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, k2, vals, v2, n, 0, end_bit, S(s));
+  void* tmp;
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, k2, vals, v2, n, 0, end_bit, S(s));  // stable: element order kept
+  cudaFreeAsync(tmp, S(s));
+  sp->con = v2;
+  sp->n_con = n;
+  // run-length encode (tile, target) -> segments
+  unsigned long long* ukeys;
+  int* counts;
+  long long* d_nseg;
+  if ((err = tmp_alloc(&ukeys, n, s)) || (err = tmp_alloc(&counts, n + 1, s)) || (err = tmp_alloc(&d_nseg, 1, s))) return err;
+  tb = 0;
+  cub::DeviceRunLengthEncode::Encode(nullptr, tb, k2, ukeys, counts, d_nseg, n, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceRunLengthEncode::Encode(tmp, tb, k2, ukeys, counts, d_nseg, n, S(s));
+  cudaFreeAsync(tmp, S(s));
+  long long nseg = 0;
+  cudaMemcpyAsync(&nseg, d_nseg, sizeof nseg, cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  sp->n_seg = nseg;
+  // segment -> contribution ranges
+  if ((err = tmp_alloc(&sp->seg_con_ptr, nseg + 1, s))) return err;
+  cudaMemsetAsync(sp->seg_con_ptr + nseg, 0, sizeof(int), S(s));
+  tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, sp->seg_con_ptr, nseg + 1, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cudaMemsetAsync(counts + nseg, 0, sizeof(int), S(s));  // counts has >= nseg + 1 slots when n > nseg
+  cub::DeviceScan::ExclusiveSum(tmp, tb, counts, sp->seg_con_ptr, nseg + 1, S(s));
+  cudaFreeAsync(tmp, S(s));
+  int* seg_tile;
+  if ((err = tmp_alloc(&seg_tile, nseg, s)) || (err = tmp_alloc(&sp->seg_target, nseg, s))) return err;
+  k_split_keys<<<grid_for(nseg, 256), 256, 0, S(s)>>>(ukeys, nseg, seg_tile, sp->seg_target);
+  if ((err = tmp_alloc(&sp->tile_seg_ptr, n_tiles + 1, s))) return err;
+  k_int_seg_ptr<<<grid_for((nseg > n_tiles + 1 ? nseg : n_tiles + 1), 256), 256, 0, S(s)>>>(seg_tile, nseg, n_tiles,
+                                                                                          sp->tile_seg_ptr);
+  cudaFreeAsync(ukeys, S(s));
+  cudaFreeAsync(counts, S(s));
+  cudaFreeAsync(d_nseg, S(s));
+  cudaFreeAsync(seg_tile, S(s));
+  cudaFreeAsync(k2, S(s));
+  // ownership: targets touched by one tile are written directly
+  int* tcount;
+  if ((err = tmp_alloc(&tcount, n_targets, s))) return err;
+  cudaMemsetAsync(tcount, 0, sizeof(int) * (n_targets ? n_targets : 1), S(s));
+  k_count_targets<<<grid_for(nseg, 256), 256, 0, S(s)>>>(sp->seg_target, nseg, tcount);
+  int *segidx, *st2, *si2, *flag, *pos;
+  if ((err = tmp_alloc(&segidx, nseg, s)) || (err = tmp_alloc(&st2, nseg, s)) || (err = tmp_alloc(&si2, nseg, s)) ||
+      (err = tmp_alloc(&flag, nseg + 1, s)) || (err = tmp_alloc(&pos, nseg + 1, s)))
+    return err;
+  k_iota<<<grid_for(nseg, 256), 256, 0, S(s)>>>(segidx, nseg);
+  tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, sp->seg_target, st2, segidx, si2, nseg, 0, bits_for(n_targets), S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceRadixSort::SortPairs(tmp, tb, sp->seg_target, st2, segidx, si2, nseg, 0, bits_for(n_targets), S(s));
+  cudaFreeAsync(tmp, S(s));
+  k_boundary_flags<<<grid_for(nseg, 256), 256, 0, S(s)>>>(st2, nseg, tcount, flag);
+  cudaMemsetAsync(flag + nseg, 0, sizeof(int), S(s));
+  tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, nseg + 1, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, nseg + 1, S(s));
+  cudaFreeAsync(tmp, S(s));
+  if ((err = tmp_alloc(&sp->seg_dst, nseg, s))) return err;
+  k_seg_dst<<<grid_for(nseg, 256), 256, 0, S(s)>>>(st2, si2, flag, pos, nseg, sp->seg_dst);
+  long long npart = 0;
+  { int v = 0; cudaMemcpyAsync(&v, pos + nseg, sizeof(int), cudaMemcpyDeviceToHost, S(s));
+    if ((err = (int)cudaStreamSynchronize(S(s)))) return err; npart = v; }
+  sp->n_partials = npart;
+  // partial targets: boundary entries of the target-sorted list, grouped by target (tile order)
+  int *btarget, *d_nb;
+  if ((err = tmp_alloc(&btarget, npart, s)) || (err = tmp_alloc(&d_nb, 1, s))) return err;
+  tb = 0;
+  cub::DeviceSelect::Flagged(nullptr, tb, st2, flag, btarget, d_nb, nseg, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceSelect::Flagged(tmp, tb, st2, flag, btarget, d_nb, nseg, S(s));
+  cudaFreeAsync(tmp, S(s));
+  int *pcounts, *d_npt;
+  if ((err = tmp_alloc(&sp->pt_target, npart, s)) || (err = tmp_alloc(&pcounts, npart + 1, s)) ||
+      (err = tmp_alloc(&d_npt, 1, s)))
+    return err;
+  tb = 0;
+  cub::DeviceRunLengthEncode::Encode(nullptr, tb, btarget, sp->pt_target, pcounts, d_npt, npart, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceRunLengthEncode::Encode(tmp, tb, btarget, sp->pt_target, pcounts, d_npt, npart, S(s));
+  cudaFreeAsync(tmp, S(s));
+  int npt = 0;
+  cudaMemcpyAsync(&npt, d_npt, sizeof(int), cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  sp->n_pt = npt;
+  if ((err = tmp_alloc(&sp->pt_ptr, (long long)npt + 1, s))) return err;
+  cudaMemsetAsync(pcounts + npt, 0, sizeof(int), S(s));
+  tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, pcounts, sp->pt_ptr, npt + 1, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, pcounts, sp->pt_ptr, npt + 1, S(s));
+  cudaFreeAsync(tmp, S(s));
+  // targets nobody writes (e.g. the diagonal block of an isolated node): zeroed every assemble
+  unsigned char* zflag;
+  int *tidx, *d_nz;
+  if ((err = tmp_alloc(&zflag, n_targets, s)) || (err = tmp_alloc(&tidx, n_targets, s)) ||
+      (err = tmp_alloc(&sp->untouched, n_targets, s)) || (err = tmp_alloc(&d_nz, 1, s)))
+    return err;
+  k_is_zero<<<grid_for(n_targets, 256), 256, 0, S(s)>>>(tcount, n_targets, zflag);
+  k_iota<<<grid_for(n_targets, 256), 256, 0, S(s)>>>(tidx, n_targets);
+  tb = 0;
+  cub::DeviceSelect::Flagged(nullptr, tb, tidx, zflag, sp->untouched, d_nz, n_targets, S(s));
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceSelect::Flagged(tmp, tb, tidx, zflag, sp->untouched, d_nz, n_targets, S(s));
+  cudaFreeAsync(tmp, S(s));
+  int nz = 0;
+  cudaMemcpyAsync(&nz, d_nz, sizeof(int), cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  sp->n_untouched = nz;
+  for (void* p : {(void*)tcount, (void*)segidx, (void*)st2, (void*)si2, (void*)flag, (void*)pos, (void*)btarget,
+                  (void*)d_nb, (void*)pcounts, (void*)d_npt, (void*)zflag, (void*)tidx, (void*)d_nz})
+    cudaFreeAsync(p, S(s));
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_rows, TilePlan* out, void* s) {
+  int err;
+  long long nh = 0, ng = 0, tiles = 0;
+  for (int k = 0; k < ne; ++k) {
+    nh += src[k].n_active * src[k].d.n_lb * src[k].d.n_lb;
+    ng += src[k].n_active * src[k].d.n_lb;
+    tiles = src[k].tile_base + (src[k].n_active + src[k].tpb - 1) / src[k].tpb;
+  }
+  out->n_tiles = tiles;
+  unsigned long long *hk, *gk;
+  unsigned *hv, *gv;
+  if ((err = tmp_alloc(&hk, nh, s)) || (err = tmp_alloc(&hv, nh, s)) || (err = tmp_alloc(&gk, ng, s)) ||
+      (err = tmp_alloc(&gv, ng, s)))
+    return err;
+  unsigned long long ph = 0, pg = 0;
+  for (int k = 0; k < ne; ++k) {
+    if (src[k].n_active > 0) {
+      k_tile_hkeys<<<grid_for(src[k].n_active, 128), 128, 0, S(s)>>>(src[k], ph, hk, hv);
+      k_tile_gkeys<<<grid_for(src[k].n_active, 128), 128, 0, S(s)>>>(src[k], pg, gk, gv);
+    }
+    ph += (unsigned long long)src[k].n_active * src[k].d.n_lb * src[k].d.n_lb;
+    pg += (unsigned long long)src[k].n_active * src[k].d.n_lb;
+  }
+  if ((err = build_segments(hk, hv, nh, tiles, n_blocks, &out->h, s))) return err;
+  if ((err = build_segments(gk, gv, ng, tiles, n_rows, &out->g, s))) return err;
+  cudaFreeAsync(hk, S(s));
+  cudaFreeAsync(hv, S(s));  // sorted copies live in SegPlan::con
+  cudaFreeAsync(gk, S(s));
+  cudaFreeAsync(gv, S(s));
+  return (int)cudaStreamSynchronize(S(s));
+}
+
+void free_tile_plan(TilePlan* p) {
+  for (SegPlan* sp : {&p->h, &p->g})
+    for (void* q : {(void*)sp->tile_seg_ptr, (void*)sp->seg_target, (void*)sp->seg_con_ptr, (void*)sp->con,
+                    (void*)sp->seg_dst, (void*)sp->pt_ptr, (void*)sp->pt_target, (void*)sp->untouched})
+      if (q) cudaFree(q);
+  *p = TilePlan{};
+}
+
+int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals, double* grad,
+               void* s) {
+  const int bb = b * b;
+  if (p.h.n_pt) k_fixup<<<grid_for(p.h.n_pt * bb, 256), 256, 0, S(s)>>>(p.h.pt_ptr, p.h.pt_target, p.h.n_pt, bb, partials, vals);
+  if (p.g.n_pt) k_fixup<<<grid_for(p.g.n_pt * b, 256), 256, 0, S(s)>>>(p.g.pt_ptr, p.g.pt_target, p.g.n_pt, b, gpartials, grad);
+  if (p.h.n_untouched) k_zero_targets<<<grid_for(p.h.n_untouched * bb, 256), 256, 0, S(s)>>>(p.h.untouched, p.h.n_untouched, bb, vals);
+  if (p.g.n_untouched) k_zero_targets<<<grid_for(p.g.n_untouched * b, 256), 256, 0, S(s)>>>(p.g.untouched, p.g.n_untouched, b, grad);
+  return (int)cudaGetLastError();
+}
+
+int tile_energy(const double* tileE, long long first, long long n, double* partial, double* out, void* s) {
+  return energy_tree(tileE + first, 1, n, partial, out, s);
+}
+
 }  // namespace symel_cuda::dev

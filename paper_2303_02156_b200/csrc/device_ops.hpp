@@ -92,21 +92,43 @@ int fp64_peak(int n_sm, double* tflops, void* stream);
 int apply_pins(const unsigned char* mask, long long n_rows, int b, const int* row_ptr, const int* col_idx,
                double* vals, double* grad, void* stream);
 
-// --- tile-deterministic reduction (K3) ------------------------------------------------------
-// see assembly_kernels.cu for the plan layout
-struct TilePlan {
-  int tile;                 // elements per tile
-  long long n_tiles;
-  int* blk_ptr = nullptr;   // per tile: [start of its unique block list] (n_tiles + 1)
-  int* blk_id = nullptr;    // unique global block ordinals per tile (sorted)
-  int* blk_dst = nullptr;   // >= 0: final block (write directly); < 0: -(partial index)-1
-  int* con_ptr = nullptr;   // per (tile, unique block): contribution range (absolute)
-  unsigned* con = nullptr;  // (element-in-tile << 10) | (li << 5) | lj
-  long long n_partials = 0;
-  int* part_ptr = nullptr;  // per boundary block: range of partial indices (in tile order)
-  int* part_blk = nullptr;  // boundary blocks
-  int* part_idx = nullptr;
-  long long n_part_blocks = 0;
+// --- tile-ordered reduction (K3) ------------------------------------------------------------
+// A tile = `tpb` consecutive active elements of one energy (one CTA of the tile kernel); tiles
+// are numbered globally in (energy, element) order. For every (tile, BSR block) pair that
+// receives contributions ("segment") the plan lists them in element order; a block touched by
+// a single tile is written directly, otherwise each tile writes a partial and the fix-up adds
+// the partials of the block in tile order. Same for gradient block rows.
+struct TileSrc {
+  const int* slots;  // per active element n_lb^2 block ordinals
+  const int* conn;
+  const int* active;
+  long long n_active;
+  long long tile_base;
+  int tpb;
+  LbDesc d;
 };
+struct SegPlan {  // one of {Hessian blocks, gradient rows}
+  long long n_seg = 0, n_con = 0, n_partials = 0, n_pt = 0, n_untouched = 0;
+  int* tile_seg_ptr = nullptr;  // n_tiles + 1
+  int* seg_target = nullptr;    // block (or row) ordinal per segment
+  int* seg_con_ptr = nullptr;   // n_seg + 1
+  unsigned* con = nullptr;      // packed (element-in-tile, local blocks)
+  int* seg_dst = nullptr;       // >= 0 final target; < 0: -(partial index) - 1
+  int* pt_ptr = nullptr;        // per partial target: range of its partials (tile order), n_pt + 1
+  int* pt_target = nullptr;
+  int* untouched = nullptr;     // targets without any contribution (zeroed every assemble)
+};
+struct TilePlan {
+  long long n_tiles = 0;
+  SegPlan h, g;
+};
+int build_tile_plan(const TileSrc* src, int n_energies, long long n_blocks, long long n_rows, TilePlan* out,
+                    void* stream);
+void free_tile_plan(TilePlan* p);
+// vals/grad for partial targets and untouched targets; deterministic (fixed order)
+int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals,
+               double* grad, void* stream);
+// fixed-order sum of per-tile energies [first, first + n) into *out
+int tile_energy(const double* tileE, long long first, long long n, double* partial, double* out, void* stream);
 
 }  // namespace symel_cuda::dev

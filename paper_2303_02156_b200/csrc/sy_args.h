@@ -22,6 +22,21 @@
     long long stage_stride;                                                              \
     int* bad_elem;                                                                       \
     double* value_out;                                                                   \
+    const int* tile_seg_ptr;                                                             \
+    const int* seg_block;                                                                \
+    const int* seg_con_ptr;                                                              \
+    const unsigned* con;                                                                 \
+    const int* seg_dst;                                                                  \
+    const int* tile_gseg_ptr;                                                            \
+    const int* gseg_row;                                                                 \
+    const int* gseg_con_ptr;                                                             \
+    const unsigned* gcon;                                                                \
+    const int* gseg_dst;                                                                 \
+    double* partials;                                                                    \
+    double* gpartials;                                                                   \
+    double* tileE;                                                                       \
+    long long tile_base;                                                                 \
+    int tile_atomic;                                                                     \
     double params[32];                                                                   \
   };
 

@@ -63,8 +63,12 @@ struct Compiled {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   int tpb = 128;
+  std::size_t smem = 0;  // dynamic shared memory per CTA
   std::string source;
 };
+
+// Elements per tile = threads per CTA of the tile kernel (one element per thread).
+constexpr int kTileElems = 128;
 
 // Kernel variants per energy.
 enum Variant : int {
@@ -122,6 +126,7 @@ struct Energy {
   double* d_elemE = nullptr;
   long long elemE_cap = 0;
   double* d_values = nullptr;  // activation / guard values per element
+  long long tile_base = 0;     // first global tile of this energy (tile plan)
 };
 
 }  // namespace
@@ -148,6 +153,11 @@ struct symel_cuda_ctx {
   bool any_pins = false;
   dev::OrderedRefs refs;
   bool refs_valid = false;
+  dev::TilePlan tplan;
+  bool tplan_valid = false;
+  double* d_partials = nullptr;
+  double* d_gpartials = nullptr;
+  double* d_tileE = nullptr;
   // scratch
   double* d_partial = nullptr;
   long long partial_cap = 0;
@@ -315,6 +325,13 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.fast = false;  // line-search guard value: exact
       s.schedule = 0;
       break;
+    case V_TILE:
+      s = base_spec(c, e, fast_tape(e));
+      s.mode = OutMode::fused_tile;
+      s.schedule = e.fact ? 2 : 1;
+      s.threads_per_block = kTileElems;
+      s.min_blocks = 2;
+      break;
     default:
       throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
   }
@@ -326,6 +343,13 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   }
   s.name = "sy_" + std::to_string(v);
   e.k[v] = compile_kernel(c, s);
+  if (v == V_TILE) {
+    const std::uint32_t n = (std::uint32_t)e.dof_slots.size();
+    e.k[v]->smem = sizeof(double) * (1 + n + n * (n + 1) / 2) * kTileElems;
+    if (c->device >= 0)
+      CK(cudaKernelSetAttributeForDevice(e.k[v]->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)e.k[v]->smem, c->device));
+  }
   return e.k[v];
 }
 
@@ -334,7 +358,8 @@ void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n) {
   if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
   const long long blocks = (n - a.t0 + k->tpb - 1) / k->tpb;
   void* params[] = {&a};
-  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, 0, c->stream));
+  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, k->smem,
+                      c->stream));
   ++c->launches;
 }
 
@@ -438,6 +463,8 @@ void build_pattern(symel_cuda_ctx* c) {
   CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
   if (c->refs_valid) dev::free_ordered_refs(&c->refs);
   c->refs_valid = false;
+  if (c->tplan_valid) dev::free_tile_plan(&c->tplan);
+  c->tplan_valid = false;
   c->pattern_dirty = false;
   cudaEventRecord(c->ev[1], c->stream);
   cudaEventSynchronize(c->ev[1]);
@@ -558,6 +585,113 @@ int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
   return v;
 }
 
+double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st);
+
+std::size_t tile_smem(const Energy& e) {
+  const std::size_t n = e.dof_slots.size();
+  return sizeof(double) * (1 + n + n * (n + 1) / 2) * kTileElems;
+}
+
+bool all_tile_capable(symel_cuda_ctx* c) {
+  for (auto& ep : c->energies) {
+    if (ep->skip) continue;
+    if (tile_smem(*ep) > 110 * 1024) return false;  // two CTAs per SM must fit (228 KB)
+  }
+  return true;
+}
+
+void ensure_tile_plan(symel_cuda_ctx* c) {
+  if (c->tplan_valid) return;
+  cudaEventRecord(c->ev[0], c->stream);
+  std::vector<dev::TileSrc> src;
+  long long tiles = 0;
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    e.tile_base = tiles;
+    if (e.skip || e.n_active == 0) continue;
+    dev::TileSrc s{};
+    s.slots = e.d_slots;
+    s.conn = c->conns[e.conn].d;
+    s.active = e.d_active;
+    s.n_active = e.n_active;
+    s.tile_base = tiles;
+    s.tpb = kTileElems;
+    s.d = lb_desc(c, e);
+    src.push_back(s);
+    tiles += (e.n_active + kTileElems - 1) / kTileElems;
+  }
+  CK(dev::build_tile_plan(src.data(), (int)src.size(), c->n_blocks, c->n_rows, &c->tplan, c->stream));
+  c->launches += 4 * src.size() + 24;
+  dalloc(&c->d_partials, (std::size_t)c->tplan.h.n_partials * c->b * c->b);
+  dalloc(&c->d_gpartials, (std::size_t)c->tplan.g.n_partials * c->b);
+  dalloc(&c->d_tileE, (std::size_t)std::max<long long>(1, tiles));
+  c->tplan_valid = true;
+  cudaEventRecord(c->ev[1], c->stream);
+  cudaEventSynchronize(c->ev[1]);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+  c->timings.pattern_ms += ms;
+}
+
+// Fast path: one tile kernel per energy (eval + in-CTA reduction), then the fixed-order
+// fix-up of shared blocks (deterministic) or nothing (atomic: per-tile red.add).
+double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
+  const int ne = (int)c->energies.size();
+  cudaEventRecord(c->ev[0], c->stream);
+  if (atomic) {
+    CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
+    CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
+  }
+  for (int q = 0; q < ne; ++q) {
+    Energy& e = *c->energies[q];
+    if (e.skip || e.n_active == 0) continue;
+    Compiled* k = kernel_for(c, e, V_TILE);
+    SyArgs a;
+    fill_args(c, e, a);
+    a.active = e.d_active;
+    a.n = e.n_active;
+    a.grad = c->d_grad;
+    a.vals = c->d_vals;
+    a.bad_elem = c->d_bad + q;
+    a.tile_seg_ptr = c->tplan.h.tile_seg_ptr;
+    a.seg_block = c->tplan.h.seg_target;
+    a.seg_con_ptr = c->tplan.h.seg_con_ptr;
+    a.con = c->tplan.h.con;
+    a.seg_dst = c->tplan.h.seg_dst;
+    a.tile_gseg_ptr = c->tplan.g.tile_seg_ptr;
+    a.gseg_row = c->tplan.g.seg_target;
+    a.gseg_con_ptr = c->tplan.g.seg_con_ptr;
+    a.gcon = c->tplan.g.con;
+    a.gseg_dst = c->tplan.g.seg_dst;
+    a.partials = c->d_partials;
+    a.gpartials = c->d_gpartials;
+    a.tileE = c->d_tileE;
+    a.tile_base = e.tile_base;
+    a.tile_atomic = atomic ? 1 : 0;
+    launch(c, k, a, e.n_active);
+  }
+  cudaEventRecord(c->ev[1], c->stream);
+  if (!atomic) {
+    CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream));
+    c->launches += 4;
+  }
+  for (int q = 0; q < ne; ++q) {
+    Energy& e = *c->energies[q];
+    if (e.skip || e.n_active == 0) continue;
+    const long long nt = (e.n_active + kTileElems - 1) / kTileElems;
+    ensure_elem_buffers(c, e, false);
+    CK(dev::tile_energy(c->d_tileE, e.tile_base, nt, c->d_partial, c->d_energy + q, c->stream));
+    c->launches += 2;
+  }
+  CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
+  ++c->launches;
+  if (c->any_pins) {
+    CK(dev::apply_pins(c->d_pins, c->n_rows, c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->d_grad, c->stream));
+    ++c->launches;
+  }
+  return finish_assemble(c, st);
+}
+
 double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st) {
   prepare(c);
   refresh_activation(c);
@@ -575,6 +709,12 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
   std::vector<int> init(ne, INT_MAX);
   CK(cudaMemcpyAsync(c->d_bad, init.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->d_energy, 0, sizeof(double) * (ne + 1), c->stream));
+  // fast modes run the tile kernel (K3) when every energy's staged element fits a CTA
+  const bool tiled = !ordered && !std::getenv("SYMEL_NO_TILE") && all_tile_capable(c);
+  if (tiled) {
+    ensure_tile_plan(c);
+    return assemble_tiled(c, atomic, st);
+  }
   if (!atomic) ensure_refs(c);
 
   cudaEventRecord(c->ev[0], c->stream);
@@ -653,6 +793,12 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     CK(dev::apply_pins(c->d_pins, c->n_rows, c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->d_grad, c->stream));
     ++c->launches;
   }
+  return finish_assemble(c, st);
+}
+
+// E + finiteness readback, timings, the check_finite contract (assembly.hpp:426-438).
+double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st) {
+  const int ne = (int)c->energies.size();
   cudaEventRecord(c->ev[2], c->stream);
   CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * ne, cudaMemcpyDeviceToHost, c->stream));
@@ -746,6 +892,8 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
     cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
     if (c->refs_valid) dev::free_ordered_refs(&c->refs);
+    if (c->tplan_valid) dev::free_tile_plan(&c->tplan);
+    cfree(c->d_partials); cfree(c->d_gpartials); cfree(c->d_tileE);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     for (auto& kv : c->kcache)
       if (kv.second->lib) cudaLibraryUnload(kv.second->lib);
@@ -1114,6 +1262,10 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
     const bool exact = mode == SYMEL_ASM_ORDERED || (e.flags & SYMEL_ENERGY_EXACT);
     KernelSpec s = base_spec(c, e, exact ? &e.deriv : fast_tape(e));
     s.mode = mode == SYMEL_ASM_ATOMIC ? OutMode::fused_atomic : OutMode::contrib;
+    if (mode != SYMEL_ASM_ORDERED && tile_smem(e) <= 110 * 1024) {
+      s.mode = OutMode::fused_tile;
+      s.threads_per_block = kTileElems;
+    }
     s.fast = !exact;
     s.schedule = exact ? 0 : (e.fact ? 2 : 1);
     const std::string src = emit_kernel(s);
@@ -1152,6 +1304,7 @@ int symel_cuda_precompile(symel_cuda_ctx* c, int eid, uint32_t flags) {
     const std::uint32_t mode = flags & 3u;
     kernel_for(c, e, mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : (mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
     if (mode != SYMEL_ASM_ORDERED) kernel_for(c, e, V_ENERGY);
+    if (mode != SYMEL_ASM_ORDERED && tile_smem(e) <= 110 * 1024) kernel_for(c, e, V_TILE);
     if (e.has_act) kernel_for(c, e, V_ACT);
     if (e.has_guard) kernel_for(c, e, V_GUARD);
   });

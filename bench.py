@@ -202,6 +202,8 @@ def main():
         A.assemble(args.mode)
     setup_s = time.time() - t_setup
     tm = A.timings()
+    plan = A.plan_info()
+    einfo = {n: A.energy_info(e) for n, e in ds.energies.items()}
 
     # ---- device-resident timed region
     clocks = ClockSampler(local)
@@ -270,7 +272,10 @@ def main():
             "config": {"workload": meta["workload"], "elements": n_elem, "mode": args.mode, "spd": spd,
                        "parallelism": f"replicas{world}",
                        "l2": "working set (BSR values + slot maps + connectivity) >> 126 MB L2; no flush needed",
-                       "pattern_ms": tm.pattern_ms, "compile_ms": tm.compile_ms, "setup_s": setup_s},
+                       "pattern_ms": tm.pattern_ms, "compile_ms": tm.compile_ms, "setup_s": setup_s,
+                       "tile_plan": plan,
+                       "kernel_ops": {n: {"tape": v["tape_ops"], "executed": v["fast_ops"], "frontier": v["frontier"]}
+                                      for n, v in einfo.items()}},
             "roofline": roof, "clocks": clk, "e2e": e2e, "gpu_launches": int(launches)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base, why = cpu_reference(args.config, 3, 1, args.ref_n)

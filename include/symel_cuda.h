@@ -159,6 +159,9 @@ typedef struct {
 } symel_cuda_energy_stats;
 /* Kernel-level facts about one energy (roofline bookkeeping). */
 int symel_cuda_energy_info(symel_cuda_ctx* ctx, int energy_id, symel_cuda_energy_stats* st);
+/* Tile-plan sizes of the last fast-path assemble: {tiles, block segments, block contributions,
+ * block partials, partial blocks, row segments, row partials, partial rows}. */
+int symel_cuda_plan_info(symel_cuda_ctx* ctx, int64_t* out8);
 /* Number of kernels launched on the device by this context since creation. */
 int symel_cuda_launch_count(symel_cuda_ctx* ctx, uint64_t* count);
 /* Compile (NVRTC, sm_100a) the kernels an assemble mode needs into the cubin cache without

@@ -1293,6 +1293,14 @@ int symel_cuda_energy_info(symel_cuda_ctx* c, int eid, symel_cuda_energy_stats* 
   });
 }
 
+int symel_cuda_plan_info(symel_cuda_ctx* c, int64_t* out8) {
+  return guarded(c, [&] {
+    const dev::TilePlan& p = c->tplan;
+    const int64_t v[8] = {p.n_tiles, p.h.n_seg, p.h.n_con, p.h.n_partials, p.h.n_pt, p.g.n_seg, p.g.n_partials, p.g.n_pt};
+    std::memcpy(out8, v, sizeof v);
+  });
+}
+
 int symel_cuda_launch_count(symel_cuda_ctx* c, uint64_t* n) {
   return guarded(c, [&] { *n = c->launches; });
 }

@@ -62,7 +62,7 @@ EXPORTS = [
     "symel_cuda_device_results", "symel_cuda_active_count", "symel_cuda_copy_active",
     "symel_cuda_element_outputs", "symel_cuda_get_timings", "symel_cuda_kernel_source",
     "symel_cuda_launch_count", "symel_cuda_fp64_peak", "symel_cuda_precompile", "symel_cuda_sync",
-    "symel_cuda_stream", "symel_cuda_energy_info",
+    "symel_cuda_stream", "symel_cuda_energy_info", "symel_cuda_plan_info",
 ]
 
 
@@ -117,6 +117,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "symel_cuda_fp64_peak": ([P, C.POINTER(D)], I),
         "symel_cuda_precompile": ([P, I, C.c_uint32], I),
         "symel_cuda_energy_info": ([P, I, C.POINTER(EnergyStats)], I),
+        "symel_cuda_plan_info": ([P, P], I),
         "symel_cuda_sync": ([P], I),
         "symel_cuda_stream": ([P, C.POINTER(P)], I),
     }
@@ -327,6 +328,13 @@ class DeviceAssembler:
         s = EnergyStats()
         self._check(self.lib.symel_cuda_energy_info(self.h, eid, C.byref(s)))
         return {k: getattr(s, k) for k, _ in EnergyStats._fields_}
+
+    def plan_info(self) -> dict:
+        v = np.zeros(8, np.int64)
+        self._check(self.lib.symel_cuda_plan_info(self.h, _ptr(v)))
+        keys = ["tiles", "block_segments", "block_contributions", "block_partials", "partial_blocks",
+                "row_segments", "row_partials", "partial_rows"]
+        return dict(zip(keys, (int(x) for x in v)))
 
     def precompile(self, eid: int, mode: str = "deterministic") -> None:
         self._check(self.lib.symel_cuda_precompile(self.h, eid, MODES[mode]))

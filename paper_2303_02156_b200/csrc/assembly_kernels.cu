@@ -503,34 +503,121 @@ int apply_pins(const unsigned char* mask, long long n_rows, int b, const int* ro
 
 namespace {
 
-// Hessian: key (global tile << 32 | block), value (element-in-tile << 10 | li << 5 | lj)
-__global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned* vals) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= src.n_active) return;
-  const int nl = src.d.n_lb;
-  const unsigned long long tile = (unsigned long long)(src.tile_base + t / src.tpb);
-  const unsigned tl = (unsigned)(t % src.tpb);
-  for (int i = 0; i < nl; ++i)
-    for (int j = 0; j < nl; ++j) {
-      const long long q = pos + (t * nl + i) * nl + j;
-      keys[q] = (tile << 32) | (unsigned)src.slots[(t * nl + i) * nl + j];
-      vals[q] = (tl << 10) | ((unsigned)i << 5) | (unsigned)j;
-    }
-}
-
-// gradient: key (global tile << 32 | block row), value (element-in-tile << 5 | li)
-__global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned* vals) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= src.n_active) return;
+// Hessian, upper BSR blocks only: each unordered local pair {i, j} contributes to the block
+// (min(gi, gj), max(gi, gj)) as the element sub-block (row side, col side); equal global blocks
+// from distinct local blocks (a repeated node) contribute both orientations to the diagonal.
+// key (global tile << 32 | block), value (position-in-tile << 10 | li << 5 | lj); unused
+// key slots hold `sentinel` and sort last.
+__global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long long sentinel,
+                             unsigned long long* keys, unsigned* vals) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= src.n_active) return;
+  const long long t = src.perm ? src.perm[p] : p;  // active ordinal at this tile position
   const long long e = src.active ? src.active[t] : t;
   const int* tup = src.conn + e * src.d.arity;
   const int nl = src.d.n_lb;
-  const unsigned long long tile = (unsigned long long)(src.tile_base + t / src.tpb);
-  const unsigned tl = (unsigned)(t % src.tpb);
-  for (int i = 0; i < nl; ++i) {
-    keys[pos + t * nl + i] = (tile << 32) | (unsigned)lb_block(src.d, tup, i);
-    vals[pos + t * nl + i] = (tl << 5) | (unsigned)i;
+  long long g[kMaxLb];
+  for (int q = 0; q < nl; ++q) g[q] = lb_block(src.d, tup, q);
+  const unsigned long long tile = (unsigned long long)(src.tile_base + p / src.tpb);
+  const unsigned tl = (unsigned)(p % src.tpb);
+  const int* sl = src.slots + t * nl * nl;
+  long long q = pos + p * nl * nl;
+  auto put = [&](int li, int lj) {
+    keys[q] = (tile << 32) | (unsigned)sl[li * nl + lj];
+    vals[q] = (tl << 10) | ((unsigned)li << 5) | (unsigned)lj;
+    ++q;
+  };
+  for (int i = 0; i < nl; ++i)
+    for (int j = i; j < nl; ++j) {
+      if (g[i] < g[j]) put(i, j);
+      else if (g[i] > g[j]) put(j, i);
+      else {
+        put(i, j);
+        if (i != j) put(j, i);
+      }
+    }
+  for (const long long q1 = pos + (p + 1) * nl * nl; q < q1; ++q) {
+    keys[q] = sentinel;
+    vals[q] = 0;
   }
+}
+
+// gradient: key (global tile << 32 | block row), value (position-in-tile << 5 | li)
+__global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned* vals) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= src.n_active) return;
+  const long long t = src.perm ? src.perm[p] : p;
+  const long long e = src.active ? src.active[t] : t;
+  const int* tup = src.conn + e * src.d.arity;
+  const int nl = src.d.n_lb;
+  const unsigned long long tile = (unsigned long long)(src.tile_base + p / src.tpb);
+  const unsigned tl = (unsigned)(p % src.tpb);
+  for (int i = 0; i < nl; ++i) {
+    keys[pos + p * nl + i] = (tile << 32) | (unsigned)lb_block(src.d, tup, i);
+    vals[pos + p * nl + i] = (tl << 5) | (unsigned)i;
+  }
+}
+
+// mirror (transposed) block of each segment's target block
+__global__ void k_seg_mirror(const int* __restrict__ target, long long n, const int* __restrict__ row_ptr,
+                             long long n_rows, const int* __restrict__ col_idx, int* __restrict__ mirror,
+                             unsigned char* __restrict__ touched) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int b = target[i];
+  long long lo = 0, hi = n_rows;  // row r: row_ptr[r] <= b < row_ptr[r + 1]
+  while (hi - lo > 1) {
+    const long long mid = (lo + hi) >> 1;
+    if (row_ptr[mid] <= b) lo = mid; else hi = mid;
+  }
+  const int m = find_block(row_ptr, col_idx, col_idx[b], lo);
+  mirror[i] = m;
+  touched[b] = 1;
+  touched[m] = 1;
+}
+
+// Morton code of an element's centroid (first three components of its local-block items)
+__device__ __forceinline__ unsigned spread10(unsigned v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void k_centroids(LbDesc d, const double* const* arrs, const int* __restrict__ conn,
+                            const int* __restrict__ active, long long n, double* __restrict__ cen) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long e = active ? active[t] : t;
+  const int* tup = conn + e * d.arity;
+  double c[3] = {0, 0, 0};
+  for (int q = 0; q < d.n_lb; ++q) {
+    const double* p = arrs[q] + (long long)tup[d.slot[q]] * d.comps[q];
+    for (int k = 0; k < 3 && k < d.comps[q]; ++k) c[k] += p[k];
+  }
+  for (int k = 0; k < 3; ++k) cen[3 * t + k] = c[k] / d.n_lb;
+}
+
+__global__ void k_morton_keys(const double* __restrict__ cen, long long n, double3 lo, double3 inv,
+                              unsigned* __restrict__ key, int* __restrict__ ord) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  auto qz = [](double v) { return (unsigned)fmin(1023.0, fmax(0.0, v)); };
+  key[t] = spread10(qz((cen[3 * t] - lo.x) * inv.x)) | (spread10(qz((cen[3 * t + 1] - lo.y) * inv.y)) << 1) |
+           (spread10(qz((cen[3 * t + 2] - lo.z) * inv.z)) << 2);
+  ord[t] = (int)t;
+}
+
+__global__ void k_compose(const int* __restrict__ perm, const int* __restrict__ active, long long n, int* __restrict__ elems) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) elems[p] = active ? active[perm[p]] : perm[p];
+}
+
+__global__ void k_not(const unsigned char* __restrict__ a, long long n, unsigned char* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = !a[i];
 }
 
 __global__ void k_split_keys(const unsigned long long* __restrict__ ukeys, long long n, int* __restrict__ seg_tile,
@@ -583,8 +670,10 @@ __global__ void k_int_seg_ptr(const int* __restrict__ keys, long long nk, long l
   if (nk == 0 && i <= nseg) ptr[i] = 0;
 }
 
-__global__ void k_fixup(const int* __restrict__ pt_ptr, const int* __restrict__ pt_target, long long n_pt, int w,
-                        const double* __restrict__ partials, double* __restrict__ out) {
+// One thread per (shared target, entry): partials of the target in (energy, tile) order; a
+// Hessian target also writes the transposed entry of its mirror (lower) block.
+__global__ void k_fixup(const int* __restrict__ pt_ptr, const int* __restrict__ pt_target, const int* __restrict__ mirror,
+                        long long n_pt, int w, int b, const double* __restrict__ partials, double* __restrict__ out) {
   const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n_pt * w) return;
   const long long p = q / w;
@@ -592,6 +681,7 @@ __global__ void k_fixup(const int* __restrict__ pt_ptr, const int* __restrict__ 
   double acc = 0.0;
   for (int k = pt_ptr[p]; k < pt_ptr[p + 1]; ++k) acc += partials[(long long)k * w + ent];
   out[(long long)pt_target[p] * w + ent] = acc;
+  if (mirror && mirror[p] != pt_target[p]) out[(long long)mirror[p] * w + (ent % b) * b + ent / b] = acc;
 }
 
 __global__ void k_zero_targets(const int* __restrict__ tg, long long n, int w, double* __restrict__ out) {
@@ -605,13 +695,18 @@ int tmp_alloc(T** p, size_t n, void* s) {
 }
 
 // Sorts (key, val) and segments it; fills the common part of a SegPlan.
+unsigned long long key_sentinel(long long n_tiles) {
+  return (1ull << (32 + bits_for((unsigned long long)n_tiles))) - 1ull;
+}
+
 int build_segments(unsigned long long* keys, unsigned* vals, long long n, long long n_tiles, long long n_targets,
-                   SegPlan* sp, void* s) {
+                   const int* row_ptr, const int* col_idx, long long n_rows, SegPlan* sp, void* s) {
   int err;
   unsigned long long* k2;
   unsigned* v2;
   if ((err = tmp_alloc(&k2, n, s)) || (err = tmp_alloc(&v2, n, s))) return err;
   const int end_bit = 32 + bits_for((unsigned long long)n_tiles);
+  const unsigned long long sentinel = key_sentinel(n_tiles);
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, k2, vals, v2, n, 0, end_bit, S(s));
   void* tmp;
@@ -633,6 +728,12 @@ int build_segments(unsigned long long* keys, unsigned* vals, long long n, long l
   long long nseg = 0;
   cudaMemcpyAsync(&nseg, d_nseg, sizeof nseg, cudaMemcpyDeviceToHost, S(s));
   if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  if (nseg > 0) {  // unused key slots (sentinel) form the last run: drop it
+    unsigned long long last = 0;
+    cudaMemcpyAsync(&last, ukeys + nseg - 1, sizeof last, cudaMemcpyDeviceToHost, S(s));
+    if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+    if (last == sentinel) --nseg;
+  }
   sp->n_seg = nseg;
   // segment -> contribution ranges
   if ((err = tmp_alloc(&sp->seg_con_ptr, nseg + 1, s))) return err;
@@ -654,6 +755,14 @@ int build_segments(unsigned long long* keys, unsigned* vals, long long n, long l
   cudaFreeAsync(d_nseg, S(s));
   cudaFreeAsync(seg_tile, S(s));
   cudaFreeAsync(k2, S(s));
+  // Hessian: mirrors (lower blocks written as transposes) and the touched mask
+  unsigned char* touched = nullptr;
+  if (row_ptr) {
+    if ((err = tmp_alloc(&sp->seg_mirror, nseg, s)) || (err = tmp_alloc(&touched, n_targets, s))) return err;
+    cudaMemsetAsync(touched, 0, n_targets ? n_targets : 1, S(s));
+    k_seg_mirror<<<grid_for(nseg, 256), 256, 0, S(s)>>>(sp->seg_target, nseg, row_ptr, n_rows, col_idx, sp->seg_mirror,
+                                                         touched);
+  }
   // ownership: targets touched by one tile are written directly
   int* tcount;
   if ((err = tmp_alloc(&tcount, n_targets, s))) return err;
@@ -716,7 +825,16 @@ int build_segments(unsigned long long* keys, unsigned* vals, long long n, long l
   if ((err = tmp_alloc(&zflag, n_targets, s)) || (err = tmp_alloc(&tidx, n_targets, s)) ||
       (err = tmp_alloc(&sp->untouched, n_targets, s)) || (err = tmp_alloc(&d_nz, 1, s)))
     return err;
-  k_is_zero<<<grid_for(n_targets, 256), 256, 0, S(s)>>>(tcount, n_targets, zflag);
+  if (touched) {
+    k_not<<<grid_for(n_targets, 256), 256, 0, S(s)>>>(touched, n_targets, zflag);
+    // partial targets also write their mirror in the fix-up
+    if ((err = tmp_alloc(&sp->pt_mirror, npt, s))) return err;
+    if (npt)
+      k_seg_mirror<<<grid_for(npt, 256), 256, 0, S(s)>>>(sp->pt_target, npt, row_ptr, n_rows, col_idx, sp->pt_mirror,
+                                                          touched);
+  } else {
+    k_is_zero<<<grid_for(n_targets, 256), 256, 0, S(s)>>>(tcount, n_targets, zflag);
+  }
   k_iota<<<grid_for(n_targets, 256), 256, 0, S(s)>>>(tidx, n_targets);
   tb = 0;
   cub::DeviceSelect::Flagged(nullptr, tb, tidx, zflag, sp->untouched, d_nz, n_targets, S(s));
@@ -730,12 +848,75 @@ int build_segments(unsigned long long* keys, unsigned* vals, long long n, long l
   for (void* p : {(void*)tcount, (void*)segidx, (void*)st2, (void*)si2, (void*)flag, (void*)pos, (void*)btarget,
                   (void*)d_nb, (void*)pcounts, (void*)d_npt, (void*)zflag, (void*)tidx, (void*)d_nz})
     cudaFreeAsync(p, S(s));
+  if (touched) cudaFreeAsync(touched, S(s));
   return (int)cudaGetLastError();
+}
+
+__global__ void k_minmax3(const double* __restrict__ a, long long items, int comps, unsigned long long* mm) {
+  // mm[0..2] = ordered-int min, mm[3..5] = ordered-int max of the first three components
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= items) return;
+  for (int c = 0; c < 3 && c < comps; ++c) {
+    const long long bits = __double_as_longlong(a[i * comps + c]);
+    const unsigned long long ord = bits < 0 ? ~(unsigned long long)bits : ((unsigned long long)bits | (1ull << 63));
+    atomicMin(mm + c, ord);
+    atomicMax(mm + 3 + c, ord);
+  }
+}
+
+double from_ordered(unsigned long long o) {
+  const unsigned long long bits = (o >> 63) ? (o & ~(1ull << 63)) : ~o;
+  double d;
+  std::memcpy(&d, &bits, 8);
+  return d;
 }
 
 }  // namespace
 
-int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_rows, TilePlan* out, void* s) {
+int tile_order(const LbDesc& d, const double* const* arrs_host, const int* conn, const int* active, long long n,
+               int* perm, int* elems, void* s) {
+  int err;
+  if (n <= 0) return 0;
+  // element centroids, their bounding box, 30-bit Morton keys
+  unsigned long long* mm;
+  const double** arrs_dev;
+  double* cen;
+  unsigned *key, *key2;
+  int* ord;
+  if ((err = tmp_alloc(&mm, 6, s)) || (err = tmp_alloc((char**)&arrs_dev, sizeof(double*) * d.n_lb, s)) ||
+      (err = tmp_alloc(&cen, 3 * n, s)) || (err = tmp_alloc(&key, n, s)) || (err = tmp_alloc(&key2, n, s)) ||
+      (err = tmp_alloc(&ord, n, s)))
+    return err;
+  const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+  cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, S(s));
+  cudaMemcpyAsync(arrs_dev, arrs_host, sizeof(double*) * d.n_lb, cudaMemcpyHostToDevice, S(s));
+  k_centroids<<<grid_for(n, 256), 256, 0, S(s)>>>(d, arrs_dev, conn, active, n, cen);
+  k_minmax3<<<grid_for(n, 256), 256, 0, S(s)>>>(cen, n, 3, mm);
+  unsigned long long h[6];
+  cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  double lo[3], inv[3];
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = from_ordered(h[c]);
+    const double ext = from_ordered(h[3 + c]) - lo[c];
+    inv[c] = ext > 0 ? 1023.0 / ext : 0.0;
+  }
+  k_morton_keys<<<grid_for(n, 256), 256, 0, S(s)>>>(cen, n, make_double3(lo[0], lo[1], lo[2]),
+                                                    make_double3(inv[0], inv[1], inv[2]), key, ord);
+  cudaFreeAsync(cen, S(s));
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, ord, perm, n, 0, 30, S(s));
+  void* tmp;
+  if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+  cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, ord, perm, n, 0, 30, S(s));  // stable: ties keep order
+  cudaFreeAsync(tmp, S(s));
+  k_compose<<<grid_for(n, 256), 256, 0, S(s)>>>(perm, active, n, elems);
+  for (void* p : {(void*)mm, (void*)arrs_dev, (void*)key, (void*)ord, (void*)key2}) cudaFreeAsync(p, S(s));
+  return (int)cudaStreamSynchronize(S(s));
+}
+
+int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_rows, const int* row_ptr,
+                    const int* col_idx, TilePlan* out, void* s) {
   int err;
   long long nh = 0, ng = 0, tiles = 0;
   for (int k = 0; k < ne; ++k) {
@@ -752,14 +933,14 @@ int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_
   unsigned long long ph = 0, pg = 0;
   for (int k = 0; k < ne; ++k) {
     if (src[k].n_active > 0) {
-      k_tile_hkeys<<<grid_for(src[k].n_active, 128), 128, 0, S(s)>>>(src[k], ph, hk, hv);
+      k_tile_hkeys<<<grid_for(src[k].n_active, 128), 128, 0, S(s)>>>(src[k], ph, key_sentinel(tiles), hk, hv);
       k_tile_gkeys<<<grid_for(src[k].n_active, 128), 128, 0, S(s)>>>(src[k], pg, gk, gv);
     }
     ph += (unsigned long long)src[k].n_active * src[k].d.n_lb * src[k].d.n_lb;
     pg += (unsigned long long)src[k].n_active * src[k].d.n_lb;
   }
-  if ((err = build_segments(hk, hv, nh, tiles, n_blocks, &out->h, s))) return err;
-  if ((err = build_segments(gk, gv, ng, tiles, n_rows, &out->g, s))) return err;
+  if ((err = build_segments(hk, hv, nh, tiles, n_blocks, row_ptr, col_idx, n_rows, &out->h, s))) return err;
+  if ((err = build_segments(gk, gv, ng, tiles, n_rows, nullptr, nullptr, 0, &out->g, s))) return err;
   cudaFreeAsync(hk, S(s));
   cudaFreeAsync(hv, S(s));  // sorted copies live in SegPlan::con
   cudaFreeAsync(gk, S(s));
@@ -770,7 +951,8 @@ int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_
 void free_tile_plan(TilePlan* p) {
   for (SegPlan* sp : {&p->h, &p->g})
     for (void* q : {(void*)sp->tile_seg_ptr, (void*)sp->seg_target, (void*)sp->seg_con_ptr, (void*)sp->con,
-                    (void*)sp->seg_dst, (void*)sp->pt_ptr, (void*)sp->pt_target, (void*)sp->untouched})
+                    (void*)sp->seg_dst, (void*)sp->pt_ptr, (void*)sp->pt_target, (void*)sp->untouched,
+                    (void*)sp->seg_mirror, (void*)sp->pt_mirror})
       if (q) cudaFree(q);
   *p = TilePlan{};
 }
@@ -778,8 +960,12 @@ void free_tile_plan(TilePlan* p) {
 int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals, double* grad,
                void* s) {
   const int bb = b * b;
-  if (p.h.n_pt) k_fixup<<<grid_for(p.h.n_pt * bb, 256), 256, 0, S(s)>>>(p.h.pt_ptr, p.h.pt_target, p.h.n_pt, bb, partials, vals);
-  if (p.g.n_pt) k_fixup<<<grid_for(p.g.n_pt * b, 256), 256, 0, S(s)>>>(p.g.pt_ptr, p.g.pt_target, p.g.n_pt, b, gpartials, grad);
+  if (p.h.n_pt)
+    k_fixup<<<grid_for(p.h.n_pt * bb, 256), 256, 0, S(s)>>>(p.h.pt_ptr, p.h.pt_target, p.h.pt_mirror, p.h.n_pt, bb, b,
+                                                            partials, vals);
+  if (p.g.n_pt)
+    k_fixup<<<grid_for(p.g.n_pt * b, 256), 256, 0, S(s)>>>(p.g.pt_ptr, p.g.pt_target, nullptr, p.g.n_pt, b, b,
+                                                           gpartials, grad);
   if (p.h.n_untouched) k_zero_targets<<<grid_for(p.h.n_untouched * bb, 256), 256, 0, S(s)>>>(p.h.untouched, p.h.n_untouched, bb, vals);
   if (p.g.n_untouched) k_zero_targets<<<grid_for(p.g.n_untouched * b, 256), 256, 0, S(s)>>>(p.g.untouched, p.g.n_untouched, b, grad);
   return (int)cudaGetLastError();

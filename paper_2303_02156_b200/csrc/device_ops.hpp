@@ -102,28 +102,36 @@ struct TileSrc {
   const int* slots;  // per active element n_lb^2 block ordinals
   const int* conn;
   const int* active;
+  const int* perm;   // tile position -> active ordinal (nullptr: identity)
   long long n_active;
   long long tile_base;
   int tpb;
   LbDesc d;
 };
+// Spatially coherent tile order: active ordinals sorted by the Morton code of the element
+// centroid (position arrays = the dof arrays of the local blocks, first 3 components, given
+// per local block in `arrs`); also returns element ids in that order.
+int tile_order(const LbDesc& d, const double* const* arrs_host, const int* conn, const int* active, long long n,
+               int* perm, int* elems, void* stream);
 struct SegPlan {  // one of {Hessian blocks, gradient rows}
   long long n_seg = 0, n_con = 0, n_partials = 0, n_pt = 0, n_untouched = 0;
   int* tile_seg_ptr = nullptr;  // n_tiles + 1
   int* seg_target = nullptr;    // block (or row) ordinal per segment
+  int* seg_mirror = nullptr;    // Hessian: transposed block (== target on the diagonal)
   int* seg_con_ptr = nullptr;   // n_seg + 1
   unsigned* con = nullptr;      // packed (element-in-tile, local blocks)
   int* seg_dst = nullptr;       // >= 0 final target; < 0: -(partial index) - 1
   int* pt_ptr = nullptr;        // per partial target: range of its partials (tile order), n_pt + 1
   int* pt_target = nullptr;
+  int* pt_mirror = nullptr;     // Hessian: transposed block of each partial target
   int* untouched = nullptr;     // targets without any contribution (zeroed every assemble)
 };
 struct TilePlan {
   long long n_tiles = 0;
   SegPlan h, g;
 };
-int build_tile_plan(const TileSrc* src, int n_energies, long long n_blocks, long long n_rows, TilePlan* out,
-                    void* stream);
+int build_tile_plan(const TileSrc* src, int n_energies, long long n_blocks, long long n_rows, const int* row_ptr,
+                    const int* col_idx, TilePlan* out, void* stream);
 void free_tile_plan(TilePlan* p);
 // vals/grad for partial targets and untouched targets; deterministic (fixed order)
 int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals,

@@ -27,6 +27,7 @@
     const int* seg_con_ptr;                                                              \
     const unsigned* con;                                                                 \
     const int* seg_dst;                                                                  \
+    const int* seg_mirror;                                                               \
     const int* tile_gseg_ptr;                                                            \
     const int* gseg_row;                                                                 \
     const int* gseg_con_ptr;                                                             \

@@ -69,6 +69,8 @@ struct Compiled {
 
 // Elements per tile = threads per CTA of the tile kernel (one element per thread).
 constexpr int kTileElems = 128;
+// Staging budget per CTA: two tile CTAs per SM (228 KB shared memory per SM on B200).
+constexpr std::size_t kTileSmemMax = 112 * 1024;
 
 // Kernel variants per energy.
 enum Variant : int {
@@ -127,6 +129,8 @@ struct Energy {
   long long elemE_cap = 0;
   double* d_values = nullptr;  // activation / guard values per element
   long long tile_base = 0;     // first global tile of this energy (tile plan)
+  int* d_tile_perm = nullptr;  // tile position -> active ordinal (Morton order)
+  int* d_tile_elems = nullptr; // tile position -> element id
 };
 
 }  // namespace
@@ -158,6 +162,7 @@ struct symel_cuda_ctx {
   double* d_partials = nullptr;
   double* d_gpartials = nullptr;
   double* d_tileE = nullptr;
+  bool last_tiled = false;
   // scratch
   double* d_partial = nullptr;
   long long partial_cap = 0;
@@ -258,6 +263,13 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
   return raw;
 }
 
+// Dynamic shared memory of the tile kernel: per element [E | g(n) | upper local-block
+// triangle of full b x b sub-blocks] (codegen.cpp stage layout), kTileElems elements.
+std::size_t tile_smem(const symel_cuda_ctx* c, const Energy& e) {
+  const std::size_t n = e.dof_slots.size(), nlb = e.bm.n_lb, bb = std::size_t(c->b) * c->b;
+  return sizeof(double) * (1 + n + bb * nlb * (nlb + 1) / 2) * kTileElems;
+}
+
 // Tape executed by the fast kernels: the factorised one when the energy has a narrowing
 // affine frontier (and is not flagged exact), else the reference tape.
 const TapeIR* fast_tape(Energy& e) {
@@ -344,8 +356,7 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   s.name = "sy_" + std::to_string(v);
   e.k[v] = compile_kernel(c, s);
   if (v == V_TILE) {
-    const std::uint32_t n = (std::uint32_t)e.dof_slots.size();
-    e.k[v]->smem = sizeof(double) * (1 + n + n * (n + 1) / 2) * kTileElems;
+    e.k[v]->smem = tile_smem(c, e);
     if (c->device >= 0)
       CK(cudaKernelSetAttributeForDevice(e.k[v]->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)e.k[v]->smem, c->device));
@@ -577,25 +588,23 @@ void ensure_elem_buffers(symel_cuda_ctx* c, Energy& e, bool contrib) {
   }
 }
 
+// Element id of the index a kernel reported: an active ordinal, or a tile position when the
+// last assemble ran the tile kernels (minimum position = deterministic, though in tile order).
 int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
-  if (!e.d_active) return t;
+  const int* map = (c->last_tiled && e.d_tile_perm) ? e.d_tile_elems : e.d_active;
+  if (!map) return t;
   int v = 0;
-  copy_sync(c, &v, e.d_active + t, sizeof(int), cudaMemcpyDeviceToHost);
-  (void)c;
+  copy_sync(c, &v, map + t, sizeof(int), cudaMemcpyDeviceToHost);
   return v;
 }
 
 double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st);
 
-std::size_t tile_smem(const Energy& e) {
-  const std::size_t n = e.dof_slots.size();
-  return sizeof(double) * (1 + n + n * (n + 1) / 2) * kTileElems;
-}
 
 bool all_tile_capable(symel_cuda_ctx* c) {
   for (auto& ep : c->energies) {
     if (ep->skip) continue;
-    if (tile_smem(*ep) > 110 * 1024) return false;  // two CTAs per SM must fit (228 KB)
+    if (tile_smem(c, *ep) > kTileSmemMax) return false;
   }
   return true;
 }
@@ -617,10 +626,30 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     s.tile_base = tiles;
     s.tpb = kTileElems;
     s.d = lb_desc(c, e);
+    // spatially coherent tiles: Morton order of element centroids (dof arrays as positions)
+    dalloc(&e.d_tile_perm, (std::size_t)e.n_active);
+    dalloc(&e.d_tile_elems, (std::size_t)e.n_active);
+    bool positions = true;
+    std::vector<const double*> arrs;
+    for (std::uint32_t q = 0; q < e.bm.n_lb; ++q) {
+      const Array& arr = c->arrays[e.bm.lb_array[q]];
+      positions = positions && arr.comps >= 3;
+      arrs.push_back(arr.d);
+    }
+    if (positions && !std::getenv("SYMEL_NO_MORTON")) {
+      CK(dev::tile_order(s.d, arrs.data(), s.conn, e.d_active, e.n_active, e.d_tile_perm, e.d_tile_elems, c->stream));
+      s.perm = e.d_tile_perm;
+      c->launches += 6;
+    } else {
+      cfree(e.d_tile_perm);
+      e.d_tile_perm = nullptr;
+      s.perm = nullptr;
+    }
     src.push_back(s);
     tiles += (e.n_active + kTileElems - 1) / kTileElems;
   }
-  CK(dev::build_tile_plan(src.data(), (int)src.size(), c->n_blocks, c->n_rows, &c->tplan, c->stream));
+  CK(dev::build_tile_plan(src.data(), (int)src.size(), c->n_blocks, c->n_rows, c->d_row_ptr, c->d_col_idx, &c->tplan,
+                          c->stream));
   c->launches += 4 * src.size() + 24;
   dalloc(&c->d_partials, (std::size_t)c->tplan.h.n_partials * c->b * c->b);
   dalloc(&c->d_gpartials, (std::size_t)c->tplan.g.n_partials * c->b);
@@ -648,7 +677,7 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     Compiled* k = kernel_for(c, e, V_TILE);
     SyArgs a;
     fill_args(c, e, a);
-    a.active = e.d_active;
+    a.active = e.d_tile_perm ? e.d_tile_elems : e.d_active;  // elements in tile order
     a.n = e.n_active;
     a.grad = c->d_grad;
     a.vals = c->d_vals;
@@ -658,6 +687,7 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     a.seg_con_ptr = c->tplan.h.seg_con_ptr;
     a.con = c->tplan.h.con;
     a.seg_dst = c->tplan.h.seg_dst;
+    a.seg_mirror = c->tplan.h.seg_mirror;
     a.tile_gseg_ptr = c->tplan.g.tile_seg_ptr;
     a.gseg_row = c->tplan.g.seg_target;
     a.gseg_con_ptr = c->tplan.g.seg_con_ptr;
@@ -711,6 +741,7 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
   CK(cudaMemsetAsync(c->d_energy, 0, sizeof(double) * (ne + 1), c->stream));
   // fast modes run the tile kernel (K3) when every energy's staged element fits a CTA
   const bool tiled = !ordered && !std::getenv("SYMEL_NO_TILE") && all_tile_capable(c);
+  c->last_tiled = tiled;
   if (tiled) {
     ensure_tile_plan(c);
     return assemble_tiled(c, atomic, st);
@@ -887,7 +918,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     for (Conn& k : c->conns) cfree(k.d);
     for (auto& e : c->energies) {
       cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
-      cfree(e->d_values);
+      cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
     cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
@@ -1262,7 +1293,7 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
     const bool exact = mode == SYMEL_ASM_ORDERED || (e.flags & SYMEL_ENERGY_EXACT);
     KernelSpec s = base_spec(c, e, exact ? &e.deriv : fast_tape(e));
     s.mode = mode == SYMEL_ASM_ATOMIC ? OutMode::fused_atomic : OutMode::contrib;
-    if (mode != SYMEL_ASM_ORDERED && tile_smem(e) <= 110 * 1024) {
+    if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
       s.mode = OutMode::fused_tile;
       s.threads_per_block = kTileElems;
     }
@@ -1312,7 +1343,7 @@ int symel_cuda_precompile(symel_cuda_ctx* c, int eid, uint32_t flags) {
     const std::uint32_t mode = flags & 3u;
     kernel_for(c, e, mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : (mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
     if (mode != SYMEL_ASM_ORDERED) kernel_for(c, e, V_ENERGY);
-    if (mode != SYMEL_ASM_ORDERED && tile_smem(e) <= 110 * 1024) kernel_for(c, e, V_TILE);
+    if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) kernel_for(c, e, V_TILE);
     if (e.has_act) kernel_for(c, e, V_ACT);
     if (e.has_guard) kernel_for(c, e, V_GUARD);
   });

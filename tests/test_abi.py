@@ -72,8 +72,10 @@ def test_codegen_sources(mode):
     ds = DeviceSystem(C.tet4_case(2), tapes=golden_tape, device=-1)
     src = ds.asm.kernel_source(ds.energies["elastic"], mode)
     assert "__global__" in src and "__launch_bounds__" in src
-    if mode == "atomic":
-        assert "atomicAdd(a.vals" in src and "atomicAdd(a.grad" in src
+    if mode == "atomic":  # the tile kernel's per-(tile, block) red.add branch
+        assert "atomicAdd(o + q" in src and "a.tile_atomic" in src
+    if mode == "deterministic":
+        assert "a.partials" in src and "__syncthreads" in src
     body = src.split("__global__")[1]
     if mode == "ordered":
         assert "sy_rcp" not in body   # IEEE division in tape order

@@ -509,7 +509,7 @@ namespace {
 // key (global tile << 32 | block), value (position-in-tile << 10 | li << 5 | lj); unused
 // key slots hold `sentinel` and sort last.
 __global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long long sentinel,
-                             unsigned long long* keys, unsigned* vals) {
+                             unsigned long long* keys, unsigned short* vals) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= src.n_active) return;
   const long long t = src.perm ? src.perm[p] : p;  // active ordinal at this tile position
@@ -522,9 +522,13 @@ __global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long 
   const unsigned tl = (unsigned)(p % src.tpb);
   const int* sl = src.slots + t * nl * nl;
   long long q = pos + p * nl * nl;
+  const int bb = src.d.b * src.d.b;
   auto put = [&](int li, int lj) {
+    const int lo = li < lj ? li : lj, hi = li < lj ? lj : li;
+    const unsigned sub = (unsigned)(lo * nl - ((lo * (lo - 1)) >> 1) + (hi - lo));
+    const unsigned off = (unsigned)(src.h0 + sub * bb) * (unsigned)src.tpb + tl;
     keys[q] = (tile << 32) | (unsigned)sl[li * nl + lj];
-    vals[q] = (tl << 10) | ((unsigned)li << 5) | (unsigned)lj;
+    vals[q] = (unsigned short)(((li > lj) ? 0x8000u : 0u) | off);
     ++q;
   };
   for (int i = 0; i < nl; ++i)
@@ -543,7 +547,7 @@ __global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long 
 }
 
 // gradient: key (global tile << 32 | block row), value (position-in-tile << 5 | li)
-__global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned* vals) {
+__global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long long* keys, unsigned short* vals) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= src.n_active) return;
   const long long t = src.perm ? src.perm[p] : p;
@@ -554,7 +558,7 @@ __global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long 
   const unsigned tl = (unsigned)(p % src.tpb);
   for (int i = 0; i < nl; ++i) {
     keys[pos + p * nl + i] = (tile << 32) | (unsigned)lb_block(src.d, tup, i);
-    vals[pos + p * nl + i] = (tl << 5) | (unsigned)i;
+    vals[pos + p * nl + i] = (unsigned short)((1u + (unsigned)(i * src.d.b)) * (unsigned)src.tpb + tl);
   }
 }
 
@@ -628,6 +632,18 @@ __global__ void k_split_keys(const unsigned long long* __restrict__ ukeys, long 
   seg_target[i] = (int)(ukeys[i] & 0xffffffffull);
 }
 
+__global__ void k_tile_max(const int* __restrict__ tile_seg_ptr, const int* __restrict__ seg_con_ptr, long long n_tiles,
+                           int* mx, int* __restrict__ tile_con_ptr) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > n_tiles) return;
+  const int s0 = tile_seg_ptr[t];
+  tile_con_ptr[t] = seg_con_ptr[s0];
+  if (t == n_tiles) return;
+  const int s1 = tile_seg_ptr[t + 1];
+  atomicMax(mx, s1 - s0);
+  atomicMax(mx + 1, seg_con_ptr[s1] - seg_con_ptr[s0]);
+}
+
 __global__ void k_count_targets(const int* __restrict__ seg_target, long long n, int* __restrict__ count) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) atomicAdd(count + seg_target[i], 1);
@@ -699,12 +715,12 @@ unsigned long long key_sentinel(long long n_tiles) {
   return (1ull << (32 + bits_for((unsigned long long)n_tiles))) - 1ull;
 }
 
-int build_segments(unsigned long long* keys, unsigned* vals, long long n, long long n_tiles, long long n_targets,
+int build_segments(unsigned long long* keys, unsigned short* vals, long long n, long long n_tiles, long long n_targets,
                    const int* row_ptr, const int* col_idx, long long n_rows, SegPlan* sp, void* s) {
   int err;
   unsigned long long* k2;
-  unsigned* v2;
-  if ((err = tmp_alloc(&k2, n, s)) || (err = tmp_alloc(&v2, n, s))) return err;
+  unsigned short* v2;
+  if ((err = tmp_alloc(&k2, n, s)) || (err = tmp_alloc(&v2, n + 2, s))) return err;
   const int end_bit = 32 + bits_for((unsigned long long)n_tiles);
   const unsigned long long sentinel = key_sentinel(n_tiles);
   size_t tb = 0;
@@ -750,6 +766,19 @@ int build_segments(unsigned long long* keys, unsigned* vals, long long n, long l
   if ((err = tmp_alloc(&sp->tile_seg_ptr, n_tiles + 1, s))) return err;
   k_int_seg_ptr<<<grid_for((nseg > n_tiles + 1 ? nseg : n_tiles + 1), 256), 256, 0, S(s)>>>(seg_tile, nseg, n_tiles,
                                                                                           sp->tile_seg_ptr);
+  {  // per-tile maxima of segments and contributions (the kernel stages a tile's plan in smem)
+    int* mx;
+    if ((err = tmp_alloc(&mx, 2, s)) || (err = tmp_alloc(&sp->tile_con_ptr, n_tiles + 1, s))) return err;
+    cudaMemsetAsync(mx, 0, 2 * sizeof(int), S(s));
+    k_tile_max<<<grid_for(n_tiles + 1, 256), 256, 0, S(s)>>>(sp->tile_seg_ptr, sp->seg_con_ptr, n_tiles, mx,
+                                                             sp->tile_con_ptr);
+    int h[2];
+    cudaMemcpyAsync(h, mx, sizeof h, cudaMemcpyDeviceToHost, S(s));
+    if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+    sp->max_tile_seg = h[0];
+    sp->max_tile_con = h[1];
+    cudaFreeAsync(mx, S(s));
+  }
   cudaFreeAsync(ukeys, S(s));
   cudaFreeAsync(counts, S(s));
   cudaFreeAsync(d_nseg, S(s));
@@ -926,7 +955,7 @@ int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_
   }
   out->n_tiles = tiles;
   unsigned long long *hk, *gk;
-  unsigned *hv, *gv;
+  unsigned short *hv, *gv;
   if ((err = tmp_alloc(&hk, nh, s)) || (err = tmp_alloc(&hv, nh, s)) || (err = tmp_alloc(&gk, ng, s)) ||
       (err = tmp_alloc(&gv, ng, s)))
     return err;
@@ -952,7 +981,7 @@ void free_tile_plan(TilePlan* p) {
   for (SegPlan* sp : {&p->h, &p->g})
     for (void* q : {(void*)sp->tile_seg_ptr, (void*)sp->seg_target, (void*)sp->seg_con_ptr, (void*)sp->con,
                     (void*)sp->seg_dst, (void*)sp->pt_ptr, (void*)sp->pt_target, (void*)sp->untouched,
-                    (void*)sp->seg_mirror, (void*)sp->pt_mirror})
+                    (void*)sp->seg_mirror, (void*)sp->pt_mirror, (void*)sp->tile_con_ptr})
       if (q) cudaFree(q);
   *p = TilePlan{};
 }

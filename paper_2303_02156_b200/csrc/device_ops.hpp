@@ -106,8 +106,12 @@ struct TileSrc {
   long long n_active;
   long long tile_base;
   int tpb;
+  int h0;            // first Hessian staging slot (1 + n_dofs); staging slot k of element tl
+                     // lives at shared double k * tpb + tl (codegen.cpp tile layout)
   LbDesc d;
 };
+// A contribution is stored as a 16-bit shared-memory double offset: Hessian
+// (transpose << 15) | ((h0 + sub(lo, hi) * b*b) * tpb + tl); gradient (1 + lb * b) * tpb + tl.
 // Spatially coherent tile order: active ordinals sorted by the Morton code of the element
 // centroid (position arrays = the dof arrays of the local blocks, first 3 components, given
 // per local block in `arrs`); also returns element ids in that order.
@@ -116,10 +120,12 @@ int tile_order(const LbDesc& d, const double* const* arrs_host, const int* conn,
 struct SegPlan {  // one of {Hessian blocks, gradient rows}
   long long n_seg = 0, n_con = 0, n_partials = 0, n_pt = 0, n_untouched = 0;
   int* tile_seg_ptr = nullptr;  // n_tiles + 1
+  int* tile_con_ptr = nullptr;  // n_tiles + 1: first contribution of each tile
   int* seg_target = nullptr;    // block (or row) ordinal per segment
   int* seg_mirror = nullptr;    // Hessian: transposed block (== target on the diagonal)
   int* seg_con_ptr = nullptr;   // n_seg + 1
-  unsigned* con = nullptr;      // packed (element-in-tile, local blocks)
+  unsigned short* con = nullptr;  // shared-memory offsets of the contributions (see TileSrc)
+  int max_tile_seg = 0, max_tile_con = 0;  // per-tile maxima (shared-memory sizing)
   int* seg_dst = nullptr;       // >= 0 final target; < 0: -(partial index) - 1
   int* pt_ptr = nullptr;        // per partial target: range of its partials (tile order), n_pt + 1
   int* pt_target = nullptr;

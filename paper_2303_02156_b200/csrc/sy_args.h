@@ -23,16 +23,22 @@
     int* bad_elem;                                                                       \
     double* value_out;                                                                   \
     const int* tile_seg_ptr;                                                             \
+    const int* tile_con_ptr;                                                             \
     const int* seg_block;                                                                \
     const int* seg_con_ptr;                                                              \
-    const unsigned* con;                                                                 \
+    const unsigned short* con;                                                           \
     const int* seg_dst;                                                                  \
     const int* seg_mirror;                                                               \
     const int* tile_gseg_ptr;                                                            \
+    const int* tile_gcon_ptr;                                                            \
     const int* gseg_row;                                                                 \
     const int* gseg_con_ptr;                                                             \
-    const unsigned* gcon;                                                                \
+    const unsigned short* gcon;                                                          \
     const int* gseg_dst;                                                                 \
+    int cap_hseg;                                                                        \
+    int cap_gseg;                                                                        \
+    int cap_hcon;                                                                        \
+    int cap_gcon;                                                                        \
     double* partials;                                                                    \
     double* gpartials;                                                                   \
     double* tileE;                                                                       \

@@ -63,14 +63,17 @@ struct Compiled {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   int tpb = 128;
-  std::size_t smem = 0;  // dynamic shared memory per CTA
+  std::size_t smem = 0;       // dynamic shared memory per CTA (tile kernel: staging part)
+  std::size_t smem_attr = 0;  // last MaxDynamicSharedMemorySize set on the kernel
   std::string source;
 };
 
 // Elements per tile = threads per CTA of the tile kernel (one element per thread).
 constexpr int kTileElems = 128;
-// Staging budget per CTA: two tile CTAs per SM (228 KB shared memory per SM on B200).
-constexpr std::size_t kTileSmemMax = 112 * 1024;
+// Shared memory per tile CTA: two CTAs per SM (228 KB per SM on B200, 1 KB reserved per CTA,
+// a little static smem). The staging part is capped lower to leave room for the plan slice.
+constexpr std::size_t kTileSmemCta = 112 * 1024;
+constexpr std::size_t kTileSmemMax = 106 * 1024;
 
 // Kernel variants per energy.
 enum Variant : int {
@@ -355,22 +358,21 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   }
   s.name = "sy_" + std::to_string(v);
   e.k[v] = compile_kernel(c, s);
-  if (v == V_TILE) {
-    e.k[v]->smem = tile_smem(c, e);
-    if (c->device >= 0)
-      CK(cudaKernelSetAttributeForDevice(e.k[v]->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)e.k[v]->smem, c->device));
-  }
+  if (v == V_TILE) e.k[v]->smem = tile_smem(c, e);  // plus the plan slice at launch
   return e.k[v];
 }
 
-void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n) {
+void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n, std::size_t smem = 0) {
   if (n <= 0) return;
   if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
   const long long blocks = (n - a.t0 + k->tpb - 1) / k->tpb;
+  if (!smem) smem = k->smem;
+  if (smem > 48 * 1024 && smem != k->smem_attr) {
+    CK(cudaKernelSetAttributeForDevice(k->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem, c->device));
+    k->smem_attr = smem;
+  }
   void* params[] = {&a};
-  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, k->smem,
-                      c->stream));
+  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, smem, c->stream));
   ++c->launches;
 }
 
@@ -626,6 +628,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     s.tile_base = tiles;
     s.tpb = kTileElems;
     s.d = lb_desc(c, e);
+    s.h0 = 1 + (int)e.dof_slots.size();
     // spatially coherent tiles: Morton order of element centroids (dof arrays as positions)
     dalloc(&e.d_tile_perm, (std::size_t)e.n_active);
     dalloc(&e.d_tile_elems, (std::size_t)e.n_active);
@@ -698,7 +701,16 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     a.tileE = c->d_tileE;
     a.tile_base = e.tile_base;
     a.tile_atomic = atomic ? 1 : 0;
-    launch(c, k, a, e.n_active);
+    a.tile_con_ptr = c->tplan.h.tile_con_ptr;
+    a.tile_gcon_ptr = c->tplan.g.tile_con_ptr;
+    a.cap_hseg = c->tplan.h.max_tile_seg + 1;
+    a.cap_gseg = c->tplan.g.max_tile_seg + 1;
+    a.cap_hcon = c->tplan.h.max_tile_con / 2 + 2;
+    a.cap_gcon = c->tplan.g.max_tile_con / 2 + 2;
+    const std::size_t plan_bytes = 4 * std::size_t(a.cap_hseg + a.cap_gseg + a.cap_hcon + a.cap_gcon);
+    if (k->smem + plan_bytes > kTileSmemCta)
+      throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': tile plan slice exceeds shared memory"};
+    launch(c, k, a, e.n_active, k->smem + plan_bytes);
   }
   cudaEventRecord(c->ev[1], c->stream);
   if (!atomic) {

@@ -215,6 +215,52 @@ def spd_project(H: np.ndarray) -> np.ndarray:
     return (V * np.maximum(w, 0.0)[..., None, :]) @ np.swapaxes(V, -1, -2)
 
 
+def assemble_spd(sysm: "System", spd_energies=None) -> dict:
+    """Oracle assembly with per-element SPD projection of the element Hessians of the listed
+    energies (default: all but inertia-like energies with n_dofs == 3 are projected too; the
+    projection of an SPD matrix is itself). E and g are unchanged by the projection; the BSR
+    values are re-accumulated from projected element blocks in (energy, element) order."""
+    base = sysm.assemble()
+    b = base["b"]
+    rp, ci = base["row_ptr"], base["col_idx"]
+    vals = np.zeros_like(base["vals"]).reshape(-1, b, b)
+    off = 0
+    layout_off = {}
+    o = 0
+    for i, a in enumerate(sysm.arrays):
+        if a["is_dof"]:
+            layout_off[i] = o
+            o += a["items"] * a["comps"]
+    for ei, e in enumerate(sysm.energies):
+        n_el = e["conn"].size // e["arity"]
+        act = base["active"][off:off + n_el].astype(bool)
+        off += n_el
+        idx = np.flatnonzero(act)
+        if idx.size == 0:
+            continue
+        nd = len(e["dof_slots"])
+        out = sysm.element_outputs(ei, 0, n_el)[idx]
+        H = out[:, 1 + nd:].reshape(-1, nd, nd)
+        if spd_energies is None or e["name"] in spd_energies:
+            H = spd_project(H)
+        conn = e["conn"].reshape(n_el, e["arity"])[idx]
+        dofs = np.zeros((idx.size, nd), np.int64)
+        for k, s in enumerate(e["dof_slots"]):
+            src = e["inputs"][s]
+            arr = sysm.arrays[src[1]]
+            dofs[:, k] = layout_off[src[1]] + conn[:, src[2]] * arr["comps"] + src[3]
+        br = dofs // b
+        # block index lookup per (row, col)
+        for k in range(nd):
+            for l in range(nd):
+                r, c = br[:, k], br[:, l]
+                blk = np.array([rp[rr] + np.searchsorted(ci[rp[rr]:rp[rr + 1]], cc) for rr, cc in zip(r, c)])
+                np.add.at(vals, (blk, dofs[:, k] % b, dofs[:, l] % b), H[:, k, l])
+    res = dict(base)
+    res["vals"] = vals.ravel()
+    return res
+
+
 def run_ref_driver(case_dir: str, backend: str = "source", threads: int = 0, lanes: int = 8, repeat: int = 1,
                    dump: bool = True, cache: str = "/tmp/symel_ref_cache", timeout: float = 3600) -> dict:
     """Runs the unmodified reference (oracle/_ref/ref_driver) on a case directory."""

@@ -1004,4 +1004,207 @@ int tile_energy(const double* tileE, long long first, long long n, double* parti
   return energy_tree(tileE + first, 1, n, partial, out, s);
 }
 
+// =================================================================== SPD projection (K2)
+//
+// Per element: H -> V max(L, 0) V^T for the symmetric n x n element Hessian (new component;
+// the reference regularises with H + tau I instead, optimizer.hpp:196-221). Eigensystem by
+// Householder tridiagonalisation + implicit QL with Wilkinson-style shifts (the classic
+// tred2 / tql2 pair, Wilkinson & Reinsch; restated here), one thread per element.
+
+namespace {
+
+template <int N>
+__device__ void sym_eig(double (&V)[N][N], double (&d)[N], double (&e)[N]) {
+  // tred2: V holds the matrix on entry, the orthogonal transformation on exit
+  for (int j = 0; j < N; ++j) d[j] = V[N - 1][j];
+  for (int i = N - 1; i > 0; --i) {
+    double scale = 0.0, h = 0.0;
+    for (int k = 0; k < i; ++k) scale += fabs(d[k]);
+    if (scale == 0.0) {
+      e[i] = d[i - 1];
+      for (int j = 0; j < i; ++j) {
+        d[j] = V[i - 1][j];
+        V[i][j] = 0.0;
+        V[j][i] = 0.0;
+      }
+    } else {
+      for (int k = 0; k < i; ++k) {
+        d[k] /= scale;
+        h += d[k] * d[k];
+      }
+      double f = d[i - 1];
+      double g = sqrt(h);
+      if (f > 0) g = -g;
+      e[i] = scale * g;
+      h -= f * g;
+      d[i - 1] = f - g;
+      for (int j = 0; j < i; ++j) e[j] = 0.0;
+      for (int j = 0; j < i; ++j) {
+        f = d[j];
+        V[j][i] = f;
+        g = e[j] + V[j][j] * f;
+        for (int k = j + 1; k <= i - 1; ++k) {
+          g += V[k][j] * d[k];
+          e[k] += V[k][j] * f;
+        }
+        e[j] = g;
+      }
+      f = 0.0;
+      for (int j = 0; j < i; ++j) {
+        e[j] /= h;
+        f += e[j] * d[j];
+      }
+      const double hh = f / (h + h);
+      for (int j = 0; j < i; ++j) e[j] -= hh * d[j];
+      for (int j = 0; j < i; ++j) {
+        f = d[j];
+        g = e[j];
+        for (int k = j; k <= i - 1; ++k) V[k][j] -= (f * e[k] + g * d[k]);
+        d[j] = V[i - 1][j];
+        V[i][j] = 0.0;
+      }
+    }
+    d[i] = h;
+  }
+  for (int i = 0; i < N - 1; ++i) {
+    V[N - 1][i] = V[i][i];
+    V[i][i] = 1.0;
+    const double h = d[i + 1];
+    if (h != 0.0) {
+      for (int k = 0; k <= i; ++k) d[k] = V[k][i + 1] / h;
+      for (int j = 0; j <= i; ++j) {
+        double g = 0.0;
+        for (int k = 0; k <= i; ++k) g += V[k][i + 1] * V[k][j];
+        for (int k = 0; k <= i; ++k) V[k][j] -= g * d[k];
+      }
+    }
+    for (int k = 0; k <= i; ++k) V[k][i + 1] = 0.0;
+  }
+  for (int j = 0; j < N; ++j) {
+    d[j] = V[N - 1][j];
+    V[N - 1][j] = 0.0;
+  }
+  V[N - 1][N - 1] = 1.0;
+  e[0] = 0.0;
+  // tql2: implicit QL on the tridiagonal (d, e), rotations accumulated into V
+  for (int i = 1; i < N; ++i) e[i - 1] = e[i];
+  e[N - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = 2.220446049250313e-16;
+  for (int l = 0; l < N; ++l) {
+    tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+    int m = l;
+    while (m < N - 1 && fabs(e[m]) > eps * tst1) ++m;
+    if (m > l) {
+      for (int iter = 0; iter < 60; ++iter) {
+        double g = d[l];
+        double p = (d[l + 1] - g) / (2.0 * e[l]);
+        double r = hypot(p, 1.0);
+        if (p < 0) r = -r;
+        d[l] = e[l] / (p + r);
+        d[l + 1] = e[l] * (p + r);
+        const double dl1 = d[l + 1];
+        double h = g - d[l];
+        for (int i = l + 2; i < N; ++i) d[i] -= h;
+        f += h;
+        p = d[m];
+        double c = 1.0, c2 = 1.0, c3 = 1.0, s = 0.0, s2 = 0.0;
+        const double el1 = e[l + 1];
+        for (int i = m - 1; i >= l; --i) {
+          c3 = c2;
+          c2 = c;
+          s2 = s;
+          g = c * e[i];
+          h = c * p;
+          r = hypot(p, e[i]);
+          e[i + 1] = s * r;
+          s = e[i] / r;
+          c = p / r;
+          p = c * d[i] - s * g;
+          d[i + 1] = h + s * (c * g + s * d[i]);
+          for (int k = 0; k < N; ++k) {
+            h = V[k][i + 1];
+            V[k][i + 1] = s * V[k][i] + c * h;
+            V[k][i] = c * V[k][i] - s * h;
+          }
+        }
+        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        e[l] = s * p;
+        d[l] = c * p;
+        if (!(fabs(e[l]) > eps * tst1)) break;
+      }
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+}
+
+// In place on the full n x n Hessian block of each element's contrib row (symmetric on exit).
+template <int N>
+__global__ void __launch_bounds__(64) k_spd_contrib(double* __restrict__ contrib, long long stride, long long off,
+                                                    long long n) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double* H = contrib + t * stride + off;
+  double V[N][N], d[N], e[N];
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) V[i][j] = 0.5 * (H[i * N + j] + H[j * N + i]);
+  sym_eig<N>(V, d, e);
+  for (int k = 0; k < N; ++k) d[k] = d[k] > 0.0 ? d[k] : 0.0;
+  for (int i = 0; i < N; ++i)
+    for (int j = i; j < N; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < N; ++k) acc += V[i][k] * d[k] * V[j][k];
+      H[i * N + j] = acc;
+      H[j * N + i] = acc;
+    }
+}
+
+// Per-element atomic scatter from contrib rows (K3' for paths that stage elements in global).
+__global__ void k_scatter_atomic(const double* __restrict__ contrib, long long stride, int nd, int nl, int b,
+                                 const signed char* __restrict__ dof_of_dummy, const int* __restrict__ slots,
+                                 const int* __restrict__ conn, const int* __restrict__ active, LbDesc d, long long n,
+                                 long long set_off_unused, double* __restrict__ vals, double* __restrict__ grad) {
+  (void)dof_of_dummy;
+  (void)set_off_unused;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double* row = contrib + t * stride;
+  const long long e = active ? active[t] : t;
+  const int* tup = conn + e * d.arity;
+  // node-major binding: dof (li, r) = li * b + r
+  for (int li = 0; li < nl; ++li) {
+    const long long g0 = d.off[li] + (long long)tup[d.slot[li]] * d.comps[li];
+    for (int r = 0; r < b; ++r) atomicAdd(grad + g0 + r, row[1 + li * b + r]);
+    for (int lj = 0; lj < nl; ++lj) {
+      double* blk = vals + (long long)slots[(t * nl + li) * nl + lj] * b * b;
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) atomicAdd(blk + r * b + c, row[1 + nd + (li * b + r) * nd + lj * b + c]);
+    }
+  }
+}
+
+}  // namespace
+
+int spd_project_contrib(double* contrib, long long stride, int n_dofs, long long n_elem, void* s) {
+  if (n_elem <= 0) return 0;
+  const long long off = 1 + n_dofs;
+  switch (n_dofs) {
+    case 3: k_spd_contrib<3><<<grid_for(n_elem, 64), 64, 0, S(s)>>>(contrib, stride, off, n_elem); break;
+    case 6: k_spd_contrib<6><<<grid_for(n_elem, 64), 64, 0, S(s)>>>(contrib, stride, off, n_elem); break;
+    case 9: k_spd_contrib<9><<<grid_for(n_elem, 64), 64, 0, S(s)>>>(contrib, stride, off, n_elem); break;
+    case 12: k_spd_contrib<12><<<grid_for(n_elem, 64), 64, 0, S(s)>>>(contrib, stride, off, n_elem); break;
+    default: return (int)cudaErrorNotSupported;
+  }
+  return (int)cudaGetLastError();
+}
+
+int scatter_atomic_contrib(const double* contrib, long long stride, int n_dofs, const LbDesc& d, const int* slots,
+                           const int* conn, const int* active, long long n, double* vals, double* grad, void* s) {
+  if (n <= 0) return 0;
+  k_scatter_atomic<<<grid_for(n, 128), 128, 0, S(s)>>>(contrib, stride, n_dofs, d.n_lb, d.b, nullptr, slots, conn,
+                                                       active, d, n, 0, vals, grad);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace symel_cuda::dev

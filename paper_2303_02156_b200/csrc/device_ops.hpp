@@ -85,6 +85,12 @@ int compact_active(const unsigned char* mask, long long n, int* active, long lon
                    void* stream);
 int min_reduce(const double* v, long long n, double* out, void* stream);
 
+// --- SPD projection (K2): in place on contrib rows [E, g(n), H(n*n)], n in {3, 6, 9, 12}
+int spd_project_contrib(double* contrib, long long stride, int n_dofs, long long n_elem, void* stream);
+// per-element red.add scatter of contrib rows into g and the BSR (node-major dof binding)
+int scatter_atomic_contrib(const double* contrib, long long stride, int n_dofs, const LbDesc& d, const int* slots,
+                           const int* conn, const int* active, long long n, double* vals, double* grad, void* stream);
+
 // --- measurement: FP64 DFMA throughput (TFLOP/s, FMA = 2 flops) over the whole device
 int fp64_peak(int n_sm, double* tflops, void* stream);
 

@@ -752,7 +752,10 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
   CK(cudaMemcpyAsync(c->d_bad, init.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->d_energy, 0, sizeof(double) * (ne + 1), c->stream));
   // fast modes run the tile kernel (K3) when every energy's staged element fits a CTA
-  const bool tiled = !ordered && !std::getenv("SYMEL_NO_TILE") && all_tile_capable(c);
+  bool any_spd = false;
+  for (auto& ep : c->energies) any_spd = any_spd || (ep->flags & SYMEL_ENERGY_SPD);
+  // the SPD projection runs as its own pass over staged element outputs (contrib path)
+  const bool tiled = !ordered && !any_spd && !std::getenv("SYMEL_NO_TILE") && all_tile_capable(c);
   c->last_tiled = tiled;
   if (tiled) {
     ensure_tile_plan(c);
@@ -768,8 +771,10 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    ensure_elem_buffers(c, e, !atomic);
-    Compiled* k = kernel_for(c, e, atomic ? V_ATOMIC : (ordered ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
+    const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
+    const bool staged = !atomic || spd;  // element outputs go through the contrib buffer
+    ensure_elem_buffers(c, e, staged);
+    Compiled* k = kernel_for(c, e, !staged ? V_ATOMIC : (ordered ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
     SyArgs a;
     fill_args(c, e, a);
     a.active = e.d_active;
@@ -781,6 +786,16 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     a.slots = e.d_slots;
     a.bad_elem = c->d_bad + q;
     launch(c, k, a, e.n_active);
+    if (spd) {  // K2: per-element projection of the element Hessian, in place
+      CK(dev::spd_project_contrib(e.d_contrib, e.deriv.n_outputs, (int)e.dof_slots.size(), e.n_active, c->stream));
+      ++c->launches;
+    }
+    if (atomic && spd) {
+      CK(dev::scatter_atomic_contrib(e.d_contrib, e.deriv.n_outputs, (int)e.dof_slots.size(), lb_desc(c, e),
+                                     e.d_slots, c->conns[e.conn].d, e.d_active, e.n_active, c->d_vals, c->d_grad,
+                                     c->stream));
+      ++c->launches;
+    }
   }
   cudaEventRecord(c->ev[1], c->stream);
   // phase 2: scatter (non-atomic), energy, pins
@@ -824,8 +839,9 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     for (int q = 0; q < ne; ++q) {
       Energy& e = *c->energies[q];
       if (e.skip || e.n_active == 0) continue;
-      const double* v = atomic ? e.d_elemE : e.d_contrib;
-      const long long stride = atomic ? 1 : e.deriv.n_outputs;
+      const bool staged = !atomic || (e.flags & SYMEL_ENERGY_SPD);
+      const double* v = staged ? e.d_contrib : e.d_elemE;
+      const long long stride = staged ? e.deriv.n_outputs : 1;
       CK(dev::energy_tree(v, stride, e.n_active, c->d_partial, c->d_energy + q, c->stream));
       c->launches += 2;
     }

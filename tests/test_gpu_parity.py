@@ -165,3 +165,20 @@ def test_gradient_translation_invariance():
     t = np.zeros((H.n_block_rows, 3))
     np.add.at(t, rows, v.sum(axis=1 + 1))  # (H 1_x)_row
     assert np.abs(t).max() <= 1e-8 * np.abs(v).max()
+
+
+@pytest.mark.parametrize("mode", ["deterministic", "atomic"])
+@pytest.mark.parametrize("name", ["tet4_c2_n6", "contact_n3"])
+def test_spd_projection(name, mode, oracle_mod):
+    """K2 (new component, parity unpinned by the reference): every element Hessian projected
+    to V max(L, 0) V^T, oracle = numpy.linalg.eigh per element."""
+    case = SMALL[name]()
+    sysm = oracle_mod.system_for_case(case, golden_tape)
+    spd_names = None if case.kind != "contact" else {"elastic", "contact"}
+    ref = oracle_mod.assemble_spd(sysm, spd_names)
+    ds = DeviceSystem(case, tapes=golden_tape, spd=True)
+    E = ds.asm.assemble(mode)
+    H = ds.asm.hessian()
+    check((E, ds.asm.gradient(), H), ref, TOL, oracle_mod)
+    w = np.linalg.eigvalsh(H.to_dense())
+    assert w.min() >= -1e-9 * max(1.0, np.abs(w).max())   # assembled SPD blocks -> PSD matrix

@@ -33,6 +33,8 @@ enum class OutMode : std::uint32_t {
   contrib = 0,   // reference layout [E, g(n), H(n*n)] per active element (exact order path)
   fused_atomic,  // E per element; g and BSR via red.global.add.f64 (nondeterministic order)
   fused_tile,    // E per element; g / BSR entries to per-element staging for the tile reducer
+  fused_tile_spd,  // tile kernel on a factorize_spd tape: in-register m x m eigen-clamp, then
+                   // H = W^T clamp(M) W staged for the tile reducer (K2 fused with K1 + K3)
   value_only,    // activation / guard kernels: single output per element (+ item reduction)
 };
 
@@ -47,7 +49,7 @@ struct KernelSpec {
   std::uint32_t b = 3;                   // BSR block size (assembly.hpp:273-276)
   OutMode mode = OutMode::contrib;
   bool fast = true;        // division strength reduction + FMA contraction
-  bool spd = false;        // per-element SPD projection of the element Hessian (new, K2)
+  std::uint32_t spd_m = 0; // fused_tile_spd: size m of the reduced eigenproblem
   int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)
   int schedule = 1;        // 0 = tape order, 1 = output-driven DFS (register-pressure aware)
   int threads_per_block = 128;

@@ -81,8 +81,20 @@ struct ZeroSimplifier {
 
 }  // namespace
 
+std::optional<TapeIR> factorize_impl(const TapeIR& t, const std::vector<std::uint32_t>& dof_slots, FactorizeInfo* info,
+                                     bool spd);
+
 std::optional<TapeIR> factorize_linear_frontier(const TapeIR& t, const std::vector<std::uint32_t>& dof_slots,
                                                 FactorizeInfo* info) {
+  return factorize_impl(t, dof_slots, info, false);
+}
+
+std::optional<TapeIR> factorize_spd(const TapeIR& t, const std::vector<std::uint32_t>& dof_slots, FactorizeInfo* info) {
+  return factorize_impl(t, dof_slots, info, true);
+}
+
+std::optional<TapeIR> factorize_impl(const TapeIR& t, const std::vector<std::uint32_t>& dof_slots, FactorizeInfo* info,
+                                     bool spd) {
   const std::uint32_t n = static_cast<std::uint32_t>(dof_slots.size());
   if (n == 0 || t.n_outputs != 1 + n + n * n) return std::nullopt;
   try {
@@ -199,6 +211,61 @@ std::optional<TapeIR> factorize_linear_frontier(const TapeIR& t, const std::vect
     roots[0] = E;
     for (std::uint32_t k = 0; k < n; ++k)
       roots[1 + k] = dot([&](std::uint32_t i) { return L[i * n + k]; }, [&](std::uint32_t i) { return dphi[i]; }, m);
+    if (spd) {
+      // R = chol(L L^T) (lower), W = R^-1 L, M = R^T phi_yy R; H = W^T M W
+      std::vector<NodeId> Gm(std::size_t(m) * m), R(std::size_t(m) * m, zero), W(std::size_t(m) * n, zero);
+      for (std::uint32_t i = 0; i < m; ++i)
+        for (std::uint32_t j = 0; j <= i; ++j)
+          Gm[i * m + j] = Gm[j * m + i] =
+              dot([&](std::uint32_t k) { return L[i * n + k]; }, [&](std::uint32_t k) { return L[j * n + k]; }, n);
+      for (std::uint32_t j = 0; j < m; ++j) {
+        NodeId s = Gm[j * m + j];
+        for (std::uint32_t k = 0; k < j; ++k)
+          if (!is_zero(R[j * m + k])) s = G.make_op(Op::sub, s, G.make_op(Op::mul, R[j * m + k], R[j * m + k]));
+        R[j * m + j] = G.make_op(Op::sqrt, s);
+        for (std::uint32_t i = j + 1; i < m; ++i) {
+          NodeId v = Gm[i * m + j];
+          for (std::uint32_t k = 0; k < j; ++k)
+            if (!is_zero(R[i * m + k]) && !is_zero(R[j * m + k]))
+              v = G.make_op(Op::sub, v, G.make_op(Op::mul, R[i * m + k], R[j * m + k]));
+          R[i * m + j] = is_zero(v) ? zero : G.make_op(Op::div, v, R[j * m + j]);
+        }
+      }
+      for (std::uint32_t i = 0; i < m; ++i)
+        for (std::uint32_t c = 0; c < n; ++c) {
+          NodeId v = L[i * n + c];
+          for (std::uint32_t k = 0; k < i; ++k)
+            if (!is_zero(R[i * m + k]) && !is_zero(W[k * n + c]))
+              v = is_zero(v) ? G.make_op(Op::neg, G.make_op(Op::mul, R[i * m + k], W[k * n + c]))
+                             : G.make_op(Op::sub, v, G.make_op(Op::mul, R[i * m + k], W[k * n + c]));
+          W[i * n + c] = is_zero(v) ? zero : G.make_op(Op::div, v, R[i * m + i]);
+        }
+      std::vector<NodeId> T(std::size_t(m) * m);  // phi_yy R
+      for (std::uint32_t i = 0; i < m; ++i)
+        for (std::uint32_t b = 0; b < m; ++b)
+          T[i * m + b] =
+              dot([&](std::uint32_t j) { return d2phi[i * m + j]; }, [&](std::uint32_t j) { return R[j * m + b]; }, m);
+      roots.resize(1 + n + std::size_t(m) * (m + 1) / 2 + std::size_t(m) * n, zero);
+      std::size_t o = 1 + n;
+      for (std::uint32_t a = 0; a < m; ++a)
+        for (std::uint32_t b = a; b < m; ++b)
+          roots[o++] = dot([&](std::uint32_t i) { return R[i * m + a]; }, [&](std::uint32_t i) { return T[i * m + b]; }, m);
+      for (std::size_t q = 0; q < W.size(); ++q) roots[o++] = W[q];
+      const symel::EvalPlan plan = symel::compress(G, roots);
+      const symel::Tape Tp = symel::lower(G, plan, t.n_inputs, n);
+      TapeIR out;
+      out.digest = t.digest;
+      out.n_inputs = Tp.n_inputs;
+      out.n_outputs = Tp.n_outputs;
+      out.n_dofs = Tp.n_dofs;
+      out.n_regs = Tp.n_regs;
+      out.consts = Tp.consts;
+      for (const symel::TapeInstr& in : Tp.instrs)
+        out.instrs.push_back({static_cast<TOp>(in.op), in.iarg, in.dst, in.a, in.b, in.c});
+      out.out_regs = Tp.out_regs;
+      if (info) *info = FactorizeInfo{m, n, t.instrs.size(), Tp.instrs.size(), nnz};
+      return out;
+    }
     for (std::uint32_t l = 0; l < n; ++l) {
       std::vector<NodeId> v(m);  // column l of phi_yy L
       for (std::uint32_t i = 0; i < m; ++i)

@@ -34,4 +34,13 @@ struct FactorizeInfo {
 std::optional<TapeIR> factorize_linear_frontier(const TapeIR& t, const std::vector<std::uint32_t>& dof_slots,
                                                 FactorizeInfo* info = nullptr);
 
+// Reduced form for the SPD projection (K2). With G = L L^T = R R^T (Cholesky) and
+// W = R^-1 L (orthonormal rows), H = W^T M W with M = R^T phi_yy R (m x m). Because W has
+// orthonormal rows, the eigen-clamp of the n x n element Hessian equals W^T clamp(M) W -- an
+// m x m eigenproblem instead of n x n, exactly. Output layout:
+//   [E, g(n), M packed upper row-major (m(m+1)/2), W row-major (m x n)]
+// (structurally zero W entries are constant-zero outputs).
+std::optional<TapeIR> factorize_spd(const TapeIR& t, const std::vector<std::uint32_t>& dof_slots,
+                                    FactorizeInfo* info = nullptr);
+
 }  // namespace symel_cuda

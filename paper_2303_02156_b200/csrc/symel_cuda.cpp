@@ -84,6 +84,7 @@ enum Variant : int {
   V_ACT,
   V_GUARD,
   V_TILE,
+  V_TILE_SPD,  // tile kernel with the fused reduced-space SPD projection
   V_COUNT
 };
 
@@ -120,6 +121,10 @@ struct Energy {
   std::optional<TapeIR> fact;
   FactorizeInfo fact_info{};
   bool fact_tried = false;
+  // reduced SPD form [E, g, M, W] of the same factorisation (factorize_spd)
+  std::optional<TapeIR> fact_spd;
+  FactorizeInfo spd_info{};
+  bool spd_tried = false;
   // runtime
   unsigned char* d_mask = nullptr;  // activation mask (all elements)
   int* d_active = nullptr;          // active list (nullptr = identity)
@@ -284,6 +289,18 @@ const TapeIR* fast_tape(Energy& e) {
   return e.fact ? &*e.fact : &e.deriv;
 }
 
+// Reduced SPD tape (nullptr when the energy cannot use the fused projection: no narrowing
+// frontier, fixed summation -- the projection must see the summed Hessian -- or exact rounding).
+const TapeIR* spd_tape(Energy& e) {
+  if (!e.spd_tried) {
+    e.spd_tried = true;
+    if (!(e.flags & SYMEL_ENERGY_EXACT) && e.n_items <= 1 && !std::getenv("SYMEL_NO_FUSED_SPD"))
+      e.fact_spd = factorize_spd(e.deriv, e.dof_slots, &e.spd_info);
+    if (e.fact_spd && (e.spd_info.frontier < 2 || e.spd_info.frontier > 9)) e.fact_spd.reset();
+  }
+  return e.fact_spd ? &*e.fact_spd : nullptr;
+}
+
 KernelSpec base_spec(symel_cuda_ctx* c, const Energy& e, const TapeIR* tape) {
   KernelSpec s;
   s.tape = tape;
@@ -347,6 +364,17 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.threads_per_block = kTileElems;
       s.min_blocks = 2;
       break;
+    case V_TILE_SPD: {
+      const TapeIR* tp = spd_tape(e);
+      if (!tp) throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': no reduced SPD form"};
+      s = base_spec(c, e, tp);
+      s.mode = OutMode::fused_tile_spd;
+      s.spd_m = e.spd_info.frontier;
+      s.schedule = 1;
+      s.threads_per_block = kTileElems;
+      s.min_blocks = 2;
+      break;
+    }
     default:
       throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
   }
@@ -358,7 +386,7 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   }
   s.name = "sy_" + std::to_string(v);
   e.k[v] = compile_kernel(c, s);
-  if (v == V_TILE) e.k[v]->smem = tile_smem(c, e);  // plus the plan slice at launch
+  if (v == V_TILE || v == V_TILE_SPD) e.k[v]->smem = tile_smem(c, e);  // plus the plan slice at launch
   return e.k[v];
 }
 
@@ -607,6 +635,7 @@ bool all_tile_capable(symel_cuda_ctx* c) {
   for (auto& ep : c->energies) {
     if (ep->skip) continue;
     if (tile_smem(c, *ep) > kTileSmemMax) return false;
+    if ((ep->flags & SYMEL_ENERGY_SPD) && !spd_tape(*ep)) return false;  // projection needs the reduced form
   }
   return true;
 }
@@ -677,7 +706,7 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    Compiled* k = kernel_for(c, e, V_TILE);
+    Compiled* k = kernel_for(c, e, (e.flags & SYMEL_ENERGY_SPD) ? V_TILE_SPD : V_TILE);
     SyArgs a;
     fill_args(c, e, a);
     a.active = e.d_tile_perm ? e.d_tile_elems : e.d_active;  // elements in tile order
@@ -755,7 +784,8 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
   bool any_spd = false;
   for (auto& ep : c->energies) any_spd = any_spd || (ep->flags & SYMEL_ENERGY_SPD);
   // the SPD projection runs as its own pass over staged element outputs (contrib path)
-  const bool tiled = !ordered && !any_spd && !std::getenv("SYMEL_NO_TILE") && all_tile_capable(c);
+  (void)any_spd;  // SPD energies run fused (V_TILE_SPD) when they have a reduced form
+  const bool tiled = !ordered && !std::getenv("SYMEL_NO_TILE") && all_tile_capable(c);
   c->last_tiled = tiled;
   if (tiled) {
     ensure_tile_plan(c);
@@ -1131,6 +1161,8 @@ int symel_cuda_set_energy_flags(symel_cuda_ctx* c, int eid, uint32_t flags) {
       for (auto& k : e.k) k = nullptr;
       e.fact.reset();
       e.fact_tried = false;
+      e.fact_spd.reset();
+      e.spd_tried = false;
     }
   });
 }
@@ -1371,7 +1403,10 @@ int symel_cuda_precompile(symel_cuda_ctx* c, int eid, uint32_t flags) {
     const std::uint32_t mode = flags & 3u;
     kernel_for(c, e, mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : (mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
     if (mode != SYMEL_ASM_ORDERED) kernel_for(c, e, V_ENERGY);
-    if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) kernel_for(c, e, V_TILE);
+    if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
+      if (!(e.flags & SYMEL_ENERGY_SPD)) kernel_for(c, e, V_TILE);
+      else if (spd_tape(e)) kernel_for(c, e, V_TILE_SPD);
+    }
     if (e.has_act) kernel_for(c, e, V_ACT);
     if (e.has_guard) kernel_for(c, e, V_GUARD);
   });

@@ -290,11 +290,12 @@ const TapeIR* fast_tape(Energy& e) {
 }
 
 // Reduced SPD tape (nullptr when the energy cannot use the fused projection: no narrowing
-// frontier, fixed summation -- the projection must see the summed Hessian -- or exact rounding).
+// frontier, or fixed summation -- the projection must see the summed Hessian).
 const TapeIR* spd_tape(Energy& e) {
   if (!e.spd_tried) {
     e.spd_tried = true;
-    if (!(e.flags & SYMEL_ENERGY_EXACT) && e.n_items <= 1 && !std::getenv("SYMEL_NO_FUSED_SPD"))
+    // exact-rounding energies also use it: kernel_for compiles them without contraction
+    if (e.n_items <= 1 && !std::getenv("SYMEL_NO_FUSED_SPD"))
       e.fact_spd = factorize_spd(e.deriv, e.dof_slots, &e.spd_info);
     if (e.fact_spd && (e.spd_info.frontier < 2 || e.spd_info.frontier > 9)) e.fact_spd.reset();
   }

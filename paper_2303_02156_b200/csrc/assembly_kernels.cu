@@ -522,13 +522,11 @@ __global__ void k_tile_hkeys(TileSrc src, unsigned long long pos, unsigned long 
   const unsigned tl = (unsigned)(p % src.tpb);
   const int* sl = src.slots + t * nl * nl;
   long long q = pos + p * nl * nl;
-  const int bb = src.d.b * src.d.b;
   auto put = [&](int li, int lj) {
     const int lo = li < lj ? li : lj, hi = li < lj ? lj : li;
     const unsigned sub = (unsigned)(lo * nl - ((lo * (lo - 1)) >> 1) + (hi - lo));
-    const unsigned off = (unsigned)(src.h0 + sub * bb) * (unsigned)src.tpb + tl;
     keys[q] = (tile << 32) | (unsigned)sl[li * nl + lj];
-    vals[q] = (unsigned short)(((li > lj) ? 0x8000u : 0u) | off);
+    vals[q] = (unsigned short)(((li > lj) ? 0x8000u : 0u) | (sub << 7) | tl);
     ++q;
   };
   for (int i = 0; i < nl; ++i)
@@ -558,7 +556,7 @@ __global__ void k_tile_gkeys(TileSrc src, unsigned long long pos, unsigned long 
   const unsigned tl = (unsigned)(p % src.tpb);
   for (int i = 0; i < nl; ++i) {
     keys[pos + p * nl + i] = (tile << 32) | (unsigned)lb_block(src.d, tup, i);
-    vals[pos + p * nl + i] = (unsigned short)((1u + (unsigned)(i * src.d.b)) * (unsigned)src.tpb + tl);
+    vals[pos + p * nl + i] = (unsigned short)(((unsigned)i << 7) | tl);
   }
 }
 

@@ -50,6 +50,7 @@ struct KernelSpec {
   OutMode mode = OutMode::contrib;
   bool fast = true;        // division strength reduction + FMA contraction
   std::uint32_t spd_m = 0; // fused_tile_spd: size m of the reduced eigenproblem
+  bool stage_global = false;  // tile modes: stage element outputs in global memory (large elements)
   int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)
   int schedule = 1;        // 0 = tape order, 1 = output-driven DFS (register-pressure aware)
   int threads_per_block = 128;

@@ -116,8 +116,9 @@ struct TileSrc {
                      // lives at shared double k * tpb + tl (codegen.cpp tile layout)
   LbDesc d;
 };
-// A contribution is stored as a 16-bit shared-memory double offset: Hessian
-// (transpose << 15) | ((h0 + sub(lo, hi) * b*b) * tpb + tl); gradient (1 + lb * b) * tpb + tl.
+// A contribution is 16 bits (tpb = 128): Hessian (transpose << 15) | (sub(lo, hi) << 7) | tl,
+// gradient (lb << 7) | tl, with tl the element's position in its tile and sub the index of the
+// staged upper local-block pair (the kernel turns them into staging offsets).
 // Spatially coherent tile order: active ordinals sorted by the Morton code of the element
 // centroid (position arrays = the dof arrays of the local blocks, first 3 components, given
 // per local block in `arrs`); also returns element ids in that order.

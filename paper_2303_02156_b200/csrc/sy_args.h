@@ -42,6 +42,7 @@
     double* partials;                                                                    \
     double* gpartials;                                                                   \
     double* tileE;                                                                       \
+    double* gstage;                                                                      \
     long long tile_base;                                                                 \
     int tile_atomic;                                                                     \
     double params[32];                                                                   \

@@ -74,6 +74,7 @@ constexpr int kTileElems = 128;
 // a little static smem). The staging part is capped lower to leave room for the plan slice.
 constexpr std::size_t kTileSmemCta = 112 * 1024;
 constexpr std::size_t kTileSmemMax = 106 * 1024;
+constexpr std::size_t kTileSmemOne = 226 * 1024;  // single CTA per SM (opt-in maximum 227 KB)
 
 // Kernel variants per energy.
 enum Variant : int {
@@ -139,6 +140,8 @@ struct Energy {
   long long tile_base = 0;     // first global tile of this energy (tile plan)
   int* d_tile_perm = nullptr;  // tile position -> active ordinal (Morton order)
   int* d_tile_elems = nullptr; // tile position -> element id
+  int cap[4] = {0, 0, 0, 0};   // shared plan-slice capacities (words): hseg, gseg, hcon, gcon
+  double* d_gstage = nullptr;  // global staging (large elements): one slab per tile
 };
 
 }  // namespace
@@ -273,9 +276,16 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
 
 // Dynamic shared memory of the tile kernel: per element [E | g(n) | upper local-block
 // triangle of full b x b sub-blocks] (codegen.cpp stage layout), kTileElems elements.
-std::size_t tile_smem(const symel_cuda_ctx* c, const Energy& e) {
+std::size_t tile_stage_doubles(const symel_cuda_ctx* c, const Energy& e) {
   const std::size_t n = e.dof_slots.size(), nlb = e.bm.n_lb, bb = std::size_t(c->b) * c->b;
-  return sizeof(double) * (1 + n + bb * nlb * (nlb + 1) / 2) * kTileElems;
+  return (1 + n + bb * nlb * (nlb + 1) / 2) * kTileElems;
+}
+// Elements whose staged outputs do not fit two CTAs per SM stage in global memory instead.
+bool tile_global_stage(const symel_cuda_ctx* c, const Energy& e) {
+  return sizeof(double) * tile_stage_doubles(c, e) > kTileSmemMax;
+}
+std::size_t tile_smem(const symel_cuda_ctx* c, const Energy& e) {
+  return tile_global_stage(c, e) ? 0 : sizeof(double) * tile_stage_doubles(c, e);
 }
 
 // Tape executed by the fast kernels: the factorised one when the energy has a narrowing
@@ -364,6 +374,7 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.schedule = e.fact ? 2 : 1;
       s.threads_per_block = kTileElems;
       s.min_blocks = 2;
+      s.stage_global = tile_global_stage(c, e);
       break;
     case V_TILE_SPD: {
       const TapeIR* tp = spd_tape(e);
@@ -374,6 +385,7 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.schedule = 1;
       s.threads_per_block = kTileElems;
       s.min_blocks = 2;
+      s.stage_global = tile_global_stage(c, e);
       break;
     }
     default:
@@ -687,6 +699,30 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
   dalloc(&c->d_partials, (std::size_t)c->tplan.h.n_partials * c->b * c->b);
   dalloc(&c->d_gpartials, (std::size_t)c->tplan.g.n_partials * c->b);
   dalloc(&c->d_tileE, (std::size_t)std::max<long long>(1, tiles));
+  // per-energy plan-slice capacities (shared memory is sized per launch)
+  std::vector<int> hs(tiles + 1), hc(tiles + 1), gs(tiles + 1), gc(tiles + 1);
+  copy_sync(c, hs.data(), c->tplan.h.tile_seg_ptr, sizeof(int) * (tiles + 1), cudaMemcpyDeviceToHost);
+  copy_sync(c, hc.data(), c->tplan.h.tile_con_ptr, sizeof(int) * (tiles + 1), cudaMemcpyDeviceToHost);
+  copy_sync(c, gs.data(), c->tplan.g.tile_seg_ptr, sizeof(int) * (tiles + 1), cudaMemcpyDeviceToHost);
+  copy_sync(c, gc.data(), c->tplan.g.tile_con_ptr, sizeof(int) * (tiles + 1), cudaMemcpyDeviceToHost);
+  for (auto& ep : c->energies) {
+    Energy& e = *ep;
+    int mx[4] = {0, 0, 0, 0};
+    const long long nt = (e.skip || e.n_active == 0) ? 0 : (e.n_active + kTileElems - 1) / kTileElems;
+    for (long long t = e.tile_base; t < e.tile_base + nt; ++t) {
+      mx[0] = std::max(mx[0], hs[t + 1] - hs[t]);
+      mx[1] = std::max(mx[1], gs[t + 1] - gs[t]);
+      mx[2] = std::max(mx[2], hc[t + 1] - hc[t]);
+      mx[3] = std::max(mx[3], gc[t + 1] - gc[t]);
+    }
+    e.cap[0] = mx[0] + 1;
+    e.cap[1] = mx[1] + 1;
+    e.cap[2] = mx[2] / 2 + 2;
+    e.cap[3] = mx[3] / 2 + 2;
+    cfree(e.d_gstage);
+    e.d_gstage = nullptr;
+    if (nt > 0 && tile_global_stage(c, e)) dalloc(&e.d_gstage, (std::size_t)nt * tile_stage_doubles(c, e));
+  }
   c->tplan_valid = true;
   cudaEventRecord(c->ev[1], c->stream);
   cudaEventSynchronize(c->ev[1]);
@@ -733,12 +769,14 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     a.tile_atomic = atomic ? 1 : 0;
     a.tile_con_ptr = c->tplan.h.tile_con_ptr;
     a.tile_gcon_ptr = c->tplan.g.tile_con_ptr;
-    a.cap_hseg = c->tplan.h.max_tile_seg + 1;
-    a.cap_gseg = c->tplan.g.max_tile_seg + 1;
-    a.cap_hcon = c->tplan.h.max_tile_con / 2 + 2;
-    a.cap_gcon = c->tplan.g.max_tile_con / 2 + 2;
+    a.cap_hseg = e.cap[0];
+    a.cap_gseg = e.cap[1];
+    a.cap_hcon = e.cap[2];
+    a.cap_gcon = e.cap[3];
+    a.gstage = e.d_gstage;
     const std::size_t plan_bytes = 4 * std::size_t(a.cap_hseg + a.cap_gseg + a.cap_hcon + a.cap_gcon);
-    if (k->smem + plan_bytes > kTileSmemCta)
+    // two CTAs per SM when staging + plan slice fit half the SM's shared memory, else one
+    if (k->smem + plan_bytes > kTileSmemOne)
       throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': tile plan slice exceeds shared memory"};
     launch(c, k, a, e.n_active, k->smem + plan_bytes);
   }
@@ -977,7 +1015,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     for (Conn& k : c->conns) cfree(k.d);
     for (auto& e : c->energies) {
       cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
-      cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems);
+      cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems); cfree(e->d_gstage);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
     cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
@@ -1357,6 +1395,7 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
     if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
       s.mode = OutMode::fused_tile;
       s.threads_per_block = kTileElems;
+      s.stage_global = tile_global_stage(c, e);
     }
     s.fast = !exact;
     s.schedule = exact ? 0 : (e.fact ? 2 : 1);

@@ -881,13 +881,23 @@ int build_segments(unsigned long long* keys, unsigned short* vals, long long n, 
 
 __global__ void k_minmax3(const double* __restrict__ a, long long items, int comps, unsigned long long* mm) {
   // mm[0..2] = ordered-int min, mm[3..5] = ordered-int max of the first three components
+  // warp-reduce first: one atomic pair per warp and component (contention-free at 6M items)
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= items) return;
   for (int c = 0; c < 3 && c < comps; ++c) {
-    const long long bits = __double_as_longlong(a[i * comps + c]);
-    const unsigned long long ord = bits < 0 ? ~(unsigned long long)bits : ((unsigned long long)bits | (1ull << 63));
-    atomicMin(mm + c, ord);
-    atomicMax(mm + 3 + c, ord);
+    unsigned long long lo = ~0ull, hi = 0ull;
+    if (i < items) {
+      const long long bits = __double_as_longlong(a[i * comps + c]);
+      lo = hi = bits < 0 ? ~(unsigned long long)bits : ((unsigned long long)bits | (1ull << 63));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = l2 < lo ? l2 : lo;
+      hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(mm + c, lo);
+      atomicMax(mm + 3 + c, hi);
+    }
   }
 }
 

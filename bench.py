@@ -190,6 +190,7 @@ def main():
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
 
+    from paper_2303_02156_b200.parallel import max_over_ranks
     from paper_2303_02156_b200.systems import DeviceSystem
 
     case = make_case(args.config)
@@ -225,10 +226,7 @@ def main():
     launches = (A.launch_count() - l0) // max(1, args.steps)
     ms = e0.elapsed_time(e1) / args.steps
     clk = clocks.stop()
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, device="cuda")
     value = world * n_elem / (ms * 1e-3) / 1e6
 
     # ---- roofline of the dominant kernel (element eval + fused assembly)
@@ -238,8 +236,15 @@ def main():
     achieved = fl / (k_ms * 1e-3) / 1e12
     roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": None, "kernel_ms": k_ms, "kernel_share_of_step": k_ms / ms,
-            "peak_source": "measured DFMA probe on this GPU (symel_cuda_fp64_peak)",
-            "algorithmic_flops_per_step": fl}
+            "peak_source": "measured DFMA probe on this GPU (symel_cuda_fp64_peak), FMA = 2 flops",
+            "algorithmic_flops_per_step": fl,
+            "flops_definition": "reference tape plan ops + accumulation (SURVEY 8(d)); SPD projection flops excluded"}
+    facts_path = os.path.join(ROOT, "profiles", "kernel_facts.json")
+    if os.path.exists(facts_path):
+        facts = json.load(open(facts_path)).get(args.config)
+        if facts and (spd or args.config != "c2"):
+            roof["traffic"] = facts["traffic_bytes"]
+            roof["ncu"] = {k: v for k, v in facts.items() if k != "traffic_bytes"}
 
     # ---- end to end through the C ABI with host buffers: H2D x, assemble, D2H E + gradient
     x_host = torch.empty(case.x.size, dtype=torch.float64, pin_memory=True)
@@ -258,10 +263,7 @@ def main():
     e3.record(stream)
     e3.synchronize()
     e2e_ms = e2.elapsed_time(e3) / args.steps
-    if dist:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms, device="cuda")
     e2e = {"value": world * n_elem / (e2e_ms * 1e-3) / 1e6, "unit": "M elements/s",
            "h2d_bytes_per_step": int(case.x.size * 8), "d2h_bytes_per_step": int(case.x.size * 8 + 8),
            "ms_per_step": e2e_ms, "note": "BSR values stay device-resident for the device PCG consumer"}

@@ -51,8 +51,12 @@ struct KernelSpec {
   bool fast = true;        // division strength reduction + FMA contraction
   std::uint32_t spd_m = 0; // fused_tile_spd: size m of the reduced eigenproblem
   bool stage_global = false;  // tile modes: stage element outputs in global memory (large elements)
+  bool plan_global = false;   // tile modes: read the plan slice from global memory (L2) instead of
+                              // prefetching it to shared memory (keeps two CTAs per SM)
   int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)
-  int schedule = 1;        // 0 = tape order, 1 = output-driven DFS (register-pressure aware)
+  int schedule = 1;        // 0 = tape order, 1 = output-driven DFS, 2 = DFS with column-major
+                           // Hessian, 3/4/5 = greedy min-live list schedule with ties broken
+                           // by the 1/2/0 order, -1 = auto (min peak live)
   int threads_per_block = 128;
   int min_blocks = 2;
   std::string name = "sy_kernel";
@@ -76,5 +80,8 @@ std::string emit_kernel(const KernelSpec& spec);
 
 // Instruction order used for emission (indices into tape->instrs).
 std::vector<std::uint32_t> schedule_instrs(const TapeIR& t, int schedule);
+int pick_schedule(const TapeIR& t);  // schedule with the lowest peak of live values
+// Peak number of simultaneously live values of an instruction order (inputs live from first use).
+std::size_t max_live(const TapeIR& t, const std::vector<std::uint32_t>& order);
 
 }  // namespace symel_cuda

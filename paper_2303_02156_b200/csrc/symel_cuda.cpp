@@ -86,6 +86,8 @@ enum Variant : int {
   V_GUARD,
   V_TILE,
   V_TILE_SPD,  // tile kernel with the fused reduced-space SPD projection
+  V_TILE_G,    // V_TILE / V_TILE_SPD reading the plan slice from L2 (slice too large for
+  V_TILE_SPD_G,  // shared memory next to the staging at two CTAs per SM)
   V_COUNT
 };
 
@@ -218,7 +220,7 @@ Energy& energy_of(symel_cuda_ctx* c, int id) {
 
 Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
   std::string src = emit_kernel(spec);
-  const std::string flags = spec.fast ? "fmad1" : "fmad0";
+  const std::string flags = "fmad1";
   const std::uint64_t key = fnv1a(src + "|" + flags + "|sm_100a|v1");
   auto it = c->kcache.find(key);
   if (it != c->kcache.end()) return it->second.get();
@@ -235,9 +237,20 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), (spec.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
       throw Fail{SYMEL_E_COMPILE, "nvrtcCreateProgram failed"};
-    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo",
-                                     spec.fast ? "--fmad=true" : "--fmad=false"};
+    // IEEE-mode tape arithmetic is emitted as __dadd_rn/__dsub_rn/__dmul_rn (codegen.cpp), so
+    // contraction is safe for the rest of every kernel
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
+    // SYMEL_PTXAS_VERBOSE=1: print ptxas register / spill usage of each compiled kernel
+    const bool verbose = std::getenv("SYMEL_PTXAS_VERBOSE") != nullptr;
+    if (verbose) opts.push_back("--ptxas-options=-v");
     const nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+    if (verbose && r == NVRTC_SUCCESS) {
+      std::size_t ls = 0;
+      nvrtcGetProgramLogSize(prog, &ls);
+      std::string log(ls, '\0');
+      nvrtcGetProgramLog(prog, log.data());
+      std::fprintf(stderr, "[symel ptxas] %s %s\n", spec.name.c_str(), log.c_str());
+    }
     if (r != NVRTC_SUCCESS) {
       std::size_t ls = 0;
       nvrtcGetProgramLogSize(prog, &ls);
@@ -326,8 +339,7 @@ KernelSpec base_spec(symel_cuda_ctx* c, const Energy& e, const TapeIR* tape) {
   return s;
 }
 
-Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
-  if (e.k[v]) return e.k[v];
+KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   KernelSpec s;
   switch (v) {
     case V_CONTRIB_IEEE:
@@ -339,12 +351,12 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
     case V_CONTRIB_FAST:
       s = base_spec(c, e, fast_tape(e));
       s.mode = OutMode::contrib;
-      s.schedule = e.fact ? 2 : 1;
+      s.schedule = -1;  // auto: lowest peak of live values
       break;
     case V_ATOMIC:
       s = base_spec(c, e, fast_tape(e));
       s.mode = OutMode::fused_atomic;
-      s.schedule = e.fact ? 2 : 1;
+      s.schedule = -1;  // auto: lowest peak of live values
       break;
     case V_ENERGY:
       s = base_spec(c, e, &e.eonly);
@@ -369,20 +381,24 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.schedule = 0;
       break;
     case V_TILE:
+    case V_TILE_G:
       s = base_spec(c, e, fast_tape(e));
+      s.plan_global = v == V_TILE_G;
       s.mode = OutMode::fused_tile;
-      s.schedule = e.fact ? 2 : 1;
+      s.schedule = -1;  // auto: lowest peak of live values
       s.threads_per_block = kTileElems;
       s.min_blocks = 2;
       s.stage_global = tile_global_stage(c, e);
       break;
-    case V_TILE_SPD: {
+    case V_TILE_SPD:
+    case V_TILE_SPD_G: {
       const TapeIR* tp = spd_tape(e);
       if (!tp) throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': no reduced SPD form"};
       s = base_spec(c, e, tp);
+      s.plan_global = v == V_TILE_SPD_G;
       s.mode = OutMode::fused_tile_spd;
       s.spd_m = e.spd_info.frontier;
-      s.schedule = 1;
+      s.schedule = -1;
       s.threads_per_block = kTileElems;
       s.min_blocks = 2;
       s.stage_global = tile_global_stage(c, e);
@@ -392,14 +408,19 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
   }
   if (e.flags & SYMEL_ENERGY_EXACT) {
-    // ill-conditioned energies: reproduce the reference's rounding (tape order, IEEE division,
-    // no contraction) in every assembly mode
+    // ill-conditioned energies: reproduce the reference's rounding (IEEE division, no
+    // contraction) in every assembly mode. The schedule only reorders SSA instructions, so it
+    // does not change any value and stays register-pressure driven.
     s.fast = false;
-    s.schedule = 0;
   }
   s.name = "sy_" + std::to_string(v);
-  e.k[v] = compile_kernel(c, s);
-  if (v == V_TILE || v == V_TILE_SPD) e.k[v]->smem = tile_smem(c, e);  // plus the plan slice at launch
+  return s;
+}
+
+Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
+  if (e.k[v]) return e.k[v];
+  e.k[v] = compile_kernel(c, spec_for(c, e, v));
+  if (v == V_TILE || v == V_TILE_SPD || v == V_TILE_G || v == V_TILE_SPD_G) e.k[v]->smem = tile_smem(c, e);  // plus the plan slice at launch
   return e.k[v];
 }
 
@@ -743,7 +764,8 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    Compiled* k = kernel_for(c, e, (e.flags & SYMEL_ENERGY_SPD) ? V_TILE_SPD : V_TILE);
+    const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
+    Compiled* k = kernel_for(c, e, spd ? V_TILE_SPD : V_TILE);
     SyArgs a;
     fill_args(c, e, a);
     a.active = e.d_tile_perm ? e.d_tile_elems : e.d_active;  // elements in tile order
@@ -774,8 +796,13 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     a.cap_hcon = e.cap[2];
     a.cap_gcon = e.cap[3];
     a.gstage = e.d_gstage;
-    const std::size_t plan_bytes = 4 * std::size_t(a.cap_hseg + a.cap_gseg + a.cap_hcon + a.cap_gcon);
-    // two CTAs per SM when staging + plan slice fit half the SM's shared memory, else one
+    std::size_t plan_bytes = 4 * std::size_t(a.cap_hseg + a.cap_gseg + a.cap_hcon + a.cap_gcon);
+    // two CTAs per SM with the plan slice prefetched to shared memory when staging + slice fit
+    // half the SM; else two CTAs reading the slice from L2 (scattered tiles: contact pairs)
+    if (k->smem + plan_bytes > kTileSmemCta && !std::getenv("SYMEL_PLAN_SMEM")) {
+      k = kernel_for(c, e, spd ? V_TILE_SPD_G : V_TILE_G);
+      plan_bytes = 0;
+    }
     if (k->smem + plan_bytes > kTileSmemOne)
       throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': tile plan slice exceeds shared memory"};
     launch(c, k, a, e.n_active, k->smem + plan_bytes);
@@ -1388,17 +1415,15 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
   return guarded(c, [&] {
     Energy& e = energy_of(c, eid);
     if (c->topology_dirty) refresh_layout(c);
+    // the kernel the assemble of this mode runs for the energy (tile kernels: plan slice in
+    // shared memory)
     const std::uint32_t mode = flags & 3u;
-    const bool exact = mode == SYMEL_ASM_ORDERED || (e.flags & SYMEL_ENERGY_EXACT);
-    KernelSpec s = base_spec(c, e, exact ? &e.deriv : fast_tape(e));
-    s.mode = mode == SYMEL_ASM_ATOMIC ? OutMode::fused_atomic : OutMode::contrib;
+    Variant v = mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : (mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : V_CONTRIB_FAST);
     if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
-      s.mode = OutMode::fused_tile;
-      s.threads_per_block = kTileElems;
-      s.stage_global = tile_global_stage(c, e);
+      if (!(e.flags & SYMEL_ENERGY_SPD)) v = V_TILE;
+      else if (spd_tape(e)) v = V_TILE_SPD;
     }
-    s.fast = !exact;
-    s.schedule = exact ? 0 : (e.fact ? 2 : 1);
+    const KernelSpec s = spec_for(c, e, v);
     const std::string src = emit_kernel(s);
     if (needed) *needed = src.size() + 1;
     if (buf && len) {

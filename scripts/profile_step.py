@@ -8,7 +8,7 @@ p.add_argument("--config", default="c2"); p.add_argument("--mode", default="dete
 p.add_argument("--spd", action="store_true")
 a = p.parse_args()
 case = {"c1": C.config1, "c2": C.config2, "c3": C.config3, "c4": C.config4, "c5": C.config5}[a.config]()
-ds = DeviceSystem(case, spd=a.spd)
+ds = DeviceSystem(case, spd=a.spd or a.config in ("c2", "c5"))
 for _ in range(a.steps):
     E = ds.asm.assemble(a.mode)
 print("E", E, "plan", ds.asm.plan_info())

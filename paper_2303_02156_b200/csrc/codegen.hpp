@@ -79,6 +79,10 @@ const char* kernel_prelude();
 std::string emit_kernel(const KernelSpec& spec);
 
 // Instruction order used for emission (indices into tape->instrs).
+// Device-source fragment of the fused SPD projection (also compiled on the host by
+// tests/test_spd_clamp.py).
+const char* eig_source();
+
 std::vector<std::uint32_t> schedule_instrs(const TapeIR& t, int schedule);
 int pick_schedule(const TapeIR& t);  // schedule with the lowest peak of live values
 // Peak number of simultaneously live values of an instruction order (inputs live from first use).

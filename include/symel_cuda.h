@@ -140,6 +140,10 @@ int symel_cuda_copy_gradient(symel_cuda_ctx* ctx, double* host);
 int symel_cuda_copy_hessian(symel_cuda_ctx* ctx, double* host_values);
 int symel_cuda_device_results(symel_cuda_ctx* ctx, const double** grad, const double** values,
                               const int32_t** row_ptr, const int32_t** col_idx);
+/* Per-energy energy sums of the last assemble / energy_only (fixed-shape tree per energy; the
+ * returned E is their sum in energy order). n must equal the number of energies. Used by the
+ * sharded multi-GPU assembly, which all-reduces the part of the elements a rank owns. */
+int symel_cuda_energy_parts(symel_cuda_ctx* ctx, double* parts, uint32_t n);
 /* Active element count of an energy (Assembler::active_count) and the active mask. */
 int symel_cuda_active_count(symel_cuda_ctx* ctx, int energy_id, uint64_t* count);
 int symel_cuda_copy_active(symel_cuda_ctx* ctx, int energy_id, uint8_t* mask);

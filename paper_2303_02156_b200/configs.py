@@ -306,6 +306,85 @@ def tet4_case(n: int = 20, seed: int = SEED_BASE + 1, stretch: float = 1.2,
     return Case(name, "tet4", x, X, tets, {"mu": mu, "lambda": lam})
 
 
+def hash_uniform(ids: np.ndarray, seed: int) -> np.ndarray:
+    """Counter-based uniform [0, 1) draws (splitmix64 of seed + id): a node's noise depends only
+    on its global id, so every rank of a sharded run regenerates the same values."""
+    with np.errstate(over="ignore"):
+        z = (np.asarray(ids, dtype=np.uint64) + np.uint64(seed)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
+@dataclasses.dataclass
+class SlabCase:
+    """One rank's part of a slab-decomposed Kuhn-grid problem (owner computes).
+
+    The global grid has world*n x n x n hexes on [0, world] x [0, 1]^2 (h = 1/n), node id
+    (i*(n+1) + j)*(n+1) + k. Rank r owns node planes [r*n, (r+1)*n) (the last rank also the
+    final plane) and the hexes whose first node v000 it owns, i.e. hex planes [r*n, (r+1)*n);
+    it also evaluates the ghost hex plane r*n - 1 whose tets touch its first owned node plane,
+    so its owned block rows are complete without any exchange. Local nodes are the planes
+    [lo_hex, (r+1)*n], in global id order."""
+    case: Case                 # local nodes, conn = own tets then ghost tets (local ids)
+    n_own: int                 # own tets (first n_own rows of case.conn)
+    row_lo: int                # owned block rows [row_lo, row_hi) in the local numbering
+    row_hi: int
+    global_ids: np.ndarray     # local node -> global node id
+
+
+def _kuhn_x_range(n: int, hex_lo: int, own_lo: int, hex_hi: int, seed: int, rel_noise: float):
+    """Hex planes [hex_lo, hex_hi) of the x-extended Kuhn grid (n x n hexes per plane), local
+    nodes = planes [hex_lo, hex_hi]; tets of [own_lo, hex_hi) first, then of [hex_lo, own_lo)."""
+    m = n + 1
+    h = 1.0 / n
+    planes = np.arange(hex_lo, hex_hi + 1)
+    pi, pj, pk = np.meshgrid(planes, np.arange(m), np.arange(m), indexing="ij")
+    gid = ((pi * m + pj) * m + pk).ravel().astype(np.int64)
+    X = np.stack([pi.ravel() * h, pj.ravel() * h, pk.ravel() * h], 1).astype(np.float64)
+    u = hash_uniform(gid[:, None] * 3 + np.arange(3)[None, :], seed)
+    x = X + (2.0 * u - 1.0) * (rel_noise * h)
+
+    def tets_of(hx):
+        hi, hj, hk = np.meshgrid(hx - hex_lo, np.arange(n), np.arange(n), indexing="ij")
+        hi, hj, hk = hi.ravel(), hj.ravel(), hk.ravel()
+
+        def v(a, b, c):
+            return ((hi + a) * m + (hj + b)) * m + (hk + c)
+
+        v000, v100, v110, v111 = v(0, 0, 0), v(1, 0, 0), v(1, 1, 0), v(1, 1, 1)
+        v101, v010, v011, v001 = v(1, 0, 1), v(0, 1, 0), v(0, 1, 1), v(0, 0, 1)
+        return np.stack([np.stack([v000, v100, v110, v111], 1), np.stack([v000, v101, v100, v111], 1),
+                         np.stack([v000, v110, v010, v111], 1), np.stack([v000, v010, v011, v111], 1),
+                         np.stack([v000, v001, v101, v111], 1), np.stack([v000, v011, v001, v111], 1)],
+                        axis=1).reshape(-1, 4).astype(np.int64)
+
+    own = tets_of(np.arange(own_lo, hex_hi))
+    ghost = tets_of(np.arange(hex_lo, own_lo))
+    return x, X, own, ghost, gid
+
+
+def tet4_slab_case(n: int, world: int, rank: int, seed: int = SEED_BASE + 2, rel_noise: float = 0.3) -> SlabCase:
+    """Config-2 material and noise amplitude on a world-times-longer grid, this rank's slab."""
+    m = n + 1
+    hex_lo = rank * n - (1 if rank > 0 else 0)
+    hex_hi = (rank + 1) * n
+    x, X, own, ghost, gid = _kuhn_x_range(n, hex_lo, rank * n, hex_hi, seed, rel_noise)
+    mu, lam = lame_from_young_poisson(NH_YOUNG, NH_POISSON)
+    case = Case(f"c2slab{rank}of{world}", "tet4", x, X, np.concatenate([own, ghost]), {"mu": mu, "lambda": lam})
+    row_lo = (rank * n - hex_lo) * m * m
+    row_hi = (hex_hi - hex_lo + (1 if rank == world - 1 else 0)) * m * m
+    return SlabCase(case, own.shape[0], row_lo, row_hi, gid)
+
+
+def tet4_global_slab_case(n: int, world: int, seed: int = SEED_BASE + 2, rel_noise: float = 0.3) -> Case:
+    """The whole world*n x n x n problem of tet4_slab_case in one piece (tests)."""
+    x, X, own, _, _ = _kuhn_x_range(n, 0, 0, world * n, seed, rel_noise)
+    mu, lam = lame_from_young_poisson(NH_YOUNG, NH_POISSON)
+    return Case(f"c2slab_global{world}", "tet4", x, X, own, {"mu": mu, "lambda": lam})
+
+
 def config1(n: int = 20) -> Case:
     return tet4_case(n, SEED_BASE + 1, 1.2, 0.02, None, "c1")
 

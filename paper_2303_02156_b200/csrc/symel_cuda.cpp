@@ -931,6 +931,12 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     }
     CK(dev::energy_serial(ptrs.data(), strides.data(), counts.data(), (int)ptrs.size(), c->d_energy + ne, c->stream));
     c->launches += 2 * ptrs.size();
+    for (int q = 0; q < ne; ++q) {  // per-energy parts (symel_cuda_energy_parts), fixed-shape trees
+      Energy& e = *c->energies[q];
+      if (e.skip || e.n_active == 0) continue;
+      CK(dev::energy_tree(e.d_contrib, e.deriv.n_outputs, e.n_active, c->d_partial, c->d_energy + q, c->stream));
+      c->launches += 2;
+    }
   } else {
     for (int q = 0; q < ne; ++q) {
       Energy& e = *c->energies[q];
@@ -1357,6 +1363,14 @@ int symel_cuda_device_results(symel_cuda_ctx* c, const double** g, const double*
     if (v) *v = c->d_vals;
     if (rp) *rp = c->d_row_ptr;
     if (ci) *ci = c->d_col_idx;
+  });
+}
+
+int symel_cuda_energy_parts(symel_cuda_ctx* c, double* parts, uint32_t n) {
+  return guarded(c, [&] {
+    if (n != c->energies.size()) throw Fail{SYMEL_E_ARG, "energy_parts: n must equal the number of energies"};
+    if (!c->d_energy) throw Fail{SYMEL_E_STATE, "energy_parts: no assemble has run"};
+    copy_sync(c, parts, c->d_energy, sizeof(double) * n, cudaMemcpyDeviceToHost);
   });
 }
 

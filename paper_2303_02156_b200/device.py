@@ -59,7 +59,7 @@ EXPORTS = [
     "symel_cuda_add_energy", "symel_cuda_set_param", "symel_cuda_set_energy_flags", "symel_cuda_set_pins",
     "symel_cuda_assemble", "symel_cuda_energy_only", "symel_cuda_guard_min", "symel_cuda_pattern_info",
     "symel_cuda_copy_pattern", "symel_cuda_copy_gradient", "symel_cuda_copy_hessian",
-    "symel_cuda_device_results", "symel_cuda_active_count", "symel_cuda_copy_active",
+    "symel_cuda_device_results", "symel_cuda_active_count", "symel_cuda_copy_active", "symel_cuda_energy_parts",
     "symel_cuda_element_outputs", "symel_cuda_get_timings", "symel_cuda_kernel_source",
     "symel_cuda_launch_count", "symel_cuda_fp64_peak", "symel_cuda_precompile", "symel_cuda_sync",
     "symel_cuda_stream", "symel_cuda_energy_info", "symel_cuda_plan_info",
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "symel_cuda_copy_hessian": ([P, P], I),
         "symel_cuda_device_results": ([P, P, P, P, P], I),
         "symel_cuda_active_count": ([P, I, C.POINTER(U64)], I),
+        "symel_cuda_energy_parts": ([P, C.POINTER(C.c_double), C.c_uint32], I),
         "symel_cuda_copy_active": ([P, I, P], I),
         "symel_cuda_element_outputs": ([P, I, U64, U64, C.c_uint32, P], I),
         "symel_cuda_get_timings": ([P, C.POINTER(Timings)], I),
@@ -303,6 +304,13 @@ class DeviceAssembler:
         v = np.empty(nb * b * b)
         self._check(self.lib.symel_cuda_copy_hessian(self.h, _ptr(v)))
         return v
+
+    def energy_parts(self) -> np.ndarray:
+        """Per-energy energy sums of the last assemble / energy_only (energy registration order)."""
+        n = len(self.energy_names)
+        out = np.zeros(n)
+        self._check(self.lib.symel_cuda_energy_parts(self.h, out.ctypes.data_as(C.POINTER(C.c_double)), n))
+        return out
 
     def active_count(self, eid: int) -> int:
         n = C.c_uint64()

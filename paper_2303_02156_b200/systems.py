@@ -92,7 +92,10 @@ class DeviceSystem:
     """A Case registered on the device; keeps array ids for updates."""
 
     def __init__(self, case: configs.Case, tapes: Optional[TapeProvider] = None, spd: bool = False,
-                 device: int = 0, Q: Optional[np.ndarray] = None):
+                 device: int = 0, Q: Optional[np.ndarray] = None, n_own: Optional[int] = None):
+        """n_own (tet4 only): the first n_own tets are owned, the rest are ghosts of a sharded
+        run (parallel.py): they are registered as a second energy "elastic_ghost" so the owned
+        energy is its own part (energy_parts) while the ghosts complete the owned block rows."""
         tapes = tapes or default_tapes()
         self.case = case
         A = self.asm = DeviceAssembler(device)
@@ -105,10 +108,17 @@ class DeviceSystem:
         self.energies: Dict[str, int] = {}
         flags = ENERGY_SPD if spd else 0
         if case.kind in ("tet4", "contact"):
+            own = case.conn if n_own is None else case.conn[:n_own]
             t = A.add_connectivity("tets", 4)
-            A.set_elements(t, case.conn)
+            A.set_elements(t, own)
             self.energies["elastic"] = A.add_energy("elastic", t, tapes("tet4_elastic"), solid_tet_inputs(self.x, self.rest),
                                                     range(12), params={24: p["mu"], 25: p["lambda"]}, flags=flags)
+            if n_own is not None and n_own < case.conn.shape[0]:
+                tg = A.add_connectivity("ghost_tets", 4)
+                A.set_elements(tg, case.conn[n_own:])
+                self.energies["elastic_ghost"] = A.add_energy(
+                    "elastic_ghost", tg, tapes("tet4_elastic"), solid_tet_inputs(self.x, self.rest), range(12),
+                    params={24: p["mu"], 25: p["lambda"]}, flags=flags)
         elif case.kind == "tet10":
             t = A.add_connectivity("tets", 10)
             A.set_elements(t, case.conn)

@@ -66,6 +66,10 @@ def lib() -> C.CDLL:
                                             C.POINTER(C.c_double)]
         _lib.oracle_guard_min.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.POINTER(C.c_double)]
         _lib.oracle_free_result.argtypes = [C.POINTER(OResult)]
+        _lib.oracle_bsr_matvec.argtypes = [C.c_int32, C.c_int64] + [C.c_void_p] * 5
+        _lib.oracle_block_jacobi_inverse.argtypes = [C.c_int32, C.c_int64] + [C.c_void_p] * 3 + [C.c_double, C.c_void_p]
+        _lib.oracle_pcg.argtypes = ([C.c_int32, C.c_int64] + [C.c_void_p] * 3 + [C.c_double, C.c_void_p, C.c_void_p,
+                                    C.c_double, C.c_int32] + [C.POINTER(C.c_int32)] * 3 + [C.POINTER(C.c_double)])
     return _lib
 
 
@@ -289,3 +293,45 @@ def rel_err(a: np.ndarray, ref: np.ndarray) -> float:
     if a.size == 0:
         return 0.0
     return float(np.max(np.abs(a - ref)) / max(1.0, float(np.max(np.abs(ref)))))
+
+
+# ---- consumer of the assembled BCRS: restated in symel_oracle.c ----------
+
+def _bsr_args(b, row_ptr, col_idx, vals):
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    return rp, ci, v, rp.size - 1
+
+
+def bsr_matvec(b: int, row_ptr, col_idx, vals, x) -> np.ndarray:
+    """BcrsMatrix::matvec (assembly.hpp:43-57), bitwise."""
+    rp, ci, v, nr = _bsr_args(b, row_ptr, col_idx, vals)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(nr * b)
+    assert lib().oracle_bsr_matvec(b, nr, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, x.ctypes.data,
+                                   y.ctypes.data) == 0
+    return y
+
+
+def block_jacobi_inverse(b: int, row_ptr, col_idx, vals, tau: float) -> np.ndarray:
+    """detail::block_jacobi_inverse (optimizer.hpp:52-90), bitwise."""
+    rp, ci, v, nr = _bsr_args(b, row_ptr, col_idx, vals)
+    inv = np.empty(nr * b * b)
+    assert lib().oracle_block_jacobi_inverse(b, nr, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, float(tau),
+                                             inv.ctypes.data) == 0
+    return inv
+
+
+def pcg(b: int, row_ptr, col_idx, vals, tau: float, rhs, rel_tol: float, max_iters: int):
+    """pcg (optimizer.hpp:119-158), bitwise; returns (x, dict(iters, converged, neg_curvature, rel_residual))."""
+    rp, ci, v, nr = _bsr_args(b, row_ptr, col_idx, vals)
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    x = np.empty(nr * b)
+    it, cv, nc = C.c_int32(), C.c_int32(), C.c_int32()
+    rr = C.c_double()
+    assert lib().oracle_pcg(b, nr, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, float(tau), rhs.ctypes.data,
+                            x.ctypes.data, float(rel_tol), int(max_iters), C.byref(it), C.byref(cv), C.byref(nc),
+                            C.byref(rr)) == 0
+    return x, {"iters": it.value, "converged": bool(cv.value), "neg_curvature": bool(nc.value),
+               "rel_residual": rr.value}

@@ -6,11 +6,13 @@
 //   * the reference's own tapes (Tape::save, tape.hpp:225-245) for every kernel,
 //   * E, gradient and the BCRS Hessian from Assembler::assemble()
 //     (assembly.hpp:108-126), plus per-element kernel outputs for a sample,
-//   * steady-state timings (the CPU baseline, `cpu_baseline.kind = "reference"`).
+//   * steady-state timings (the CPU baseline, `cpu_baseline.kind = "reference"`),
+//   * with --solver: the reference's BcrsMatrix::matvec (assembly.hpp:43-57), block-Jacobi
+//     inverse and pcg (optimizer.hpp:52-158) on the assembled Hessian (solver fixtures).
 // Built by oracle/Makefile into oracle/_ref/ref_driver.
 //
 // usage: ref_driver CASE_DIR [--backend interp|source] [--threads T] [--lanes W]
-//                   [--repeat K] [--no-dump] [--cache DIR] [--elem-sample N]
+//                   [--repeat K] [--no-dump] [--cache DIR] [--elem-sample N] [--solver]
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -25,6 +27,7 @@
 #include "symel/assembly.hpp"
 #include "symel/energies.hpp"
 #include "symel/mesh_io.hpp"
+#include "symel/optimizer.hpp"
 
 using namespace symel;
 
@@ -82,7 +85,7 @@ int main(int argc, char** argv) {
   std::string backend = "source", cache_dir = "/tmp/symel_ref_cache";
   int threads = static_cast<int>(std::thread::hardware_concurrency());
   int lanes = 8, repeat = 1;
-  bool dump = true;
+  bool dump = true, solver = false;
   std::size_t elem_sample = 64;
   for (int i = 2; i < argc; ++i) {
     std::string a = argv[i];
@@ -94,6 +97,7 @@ int main(int argc, char** argv) {
     else if (a == "--no-dump") dump = false;
     else if (a == "--cache") cache_dir = next();
     else if (a == "--elem-sample") elem_sample = std::stoul(next());
+    else if (a == "--solver") solver = true;
     else { std::fprintf(stderr, "unknown option %s\n", a.c_str()); return 2; }
   }
   try {
@@ -253,6 +257,38 @@ int main(int argc, char** argv) {
     write_bin("ref_rowptr.i64", rp.data(), rp.size());
     write_bin("ref_colidx.i64", ci.data(), ci.size());
     write_bin("ref_vals.f64", H.values.data(), H.values.size());
+    if (solver) {
+      // probe vector, y = H probe; block-Jacobi inverses and PCG (rhs = -g) for three shifts
+      const std::size_t n = H.n_rows();
+      std::vector<double> probe(n), y(n);
+      for (std::size_t i = 0; i < n; ++i) probe[i] = 1.0 + 0.5 * std::sin(0.37 * double(i)) - 0.25 * double(i % 7) / 7.0;
+      H.matvec(probe, y, 1);
+      write_bin("ref_probe.f64", probe.data(), n);
+      write_bin("ref_matvec.f64", y.data(), n);
+      double dmax = 0.0;
+      for (std::size_t r = 0; r < H.n_block_rows; ++r) {
+        const double* v = H.block(H.find_block(r, r));
+        for (int i = 0; i < H.b; ++i) dmax = std::max(dmax, std::abs(v[i * H.b + i]));
+      }
+      const double taus[3] = {0.0, 0.1 * dmax, 10.0 * dmax};
+      write_bin("ref_pcg_taus.f64", taus, 3);
+      std::vector<double> rhs(n), x(n), inv;
+      for (std::size_t i = 0; i < n; ++i) rhs[i] = -as.gradient()[i];
+      std::ofstream ps(g_dir + "/ref_pcg.txt");
+      for (int t = 0; t < 3; ++t) {
+        detail::block_jacobi_inverse(H, taus[t], inv);
+        write_bin("ref_bjinv_" + std::to_string(t) + ".f64", inv.data(), inv.size());
+        for (const double tol : {1e-4, 1e-10}) {
+          const PcgResult pr = pcg(H, taus[t], rhs, x, tol, static_cast<int>(n), 1);
+          const std::string tag = std::to_string(t) + (tol > 1e-6 ? "_loose" : "_tight");
+          write_bin("ref_pcg_x_" + tag + ".f64", x.data(), n);
+          char buf[256];
+          std::snprintf(buf, sizeof buf, "%s %d %d %d %.17g\n", tag.c_str(), pr.iters, int(pr.converged),
+                        int(pr.neg_curvature), pr.rel_residual);
+          ps << buf;
+        }
+      }
+    }
     std::ofstream st(g_dir + "/ref_stats.txt");
     st << "b " << H.b << "\n";
     for (std::size_t d = 0; d < sys.n_energies(); ++d) {

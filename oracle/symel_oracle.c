@@ -450,3 +450,133 @@ void oracle_free_result(oracle_result* r) {
   free(r->row_ptr); free(r->col_idx); free(r->vals); free(r->grad); free(r->active);
   memset(r, 0, sizeof *r);
 }
+
+/* ---- consumer of the assembled BCRS: SpMV, block-Jacobi, PCG ---- */
+
+/* y = A x, BcrsMatrix::matvec (assembly.hpp:43-57): per block row, blocks in stored order,
+ * acc[i] += v[i*b+j] * x[col*b+j] from 0.0. */
+int oracle_bsr_matvec(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci, const double* vals,
+                      const double* x, double* y) {
+  if (b < 1 || b > 4) return 1;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    double acc[16] = {0};
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+      const double* v = vals + k * b * b;
+      const double* xc = x + ci[k] * b;
+      for (int i = 0; i < b; ++i)
+        for (int j = 0; j < b; ++j) acc[i] += v[i * b + j] * xc[j];
+    }
+    for (int i = 0; i < b; ++i) y[r * b + i] = acc[i];
+  }
+  return 0;
+}
+
+/* detail::block_jacobi_inverse (optimizer.hpp:52-90): inverse of each diagonal block + tau I by
+ * the adjugate; missing block or unusable determinant -> identity; b = 1: 1/d or 1. */
+int oracle_block_jacobi_inverse(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci,
+                                const double* vals, double tau, double* inv) {
+  if (b != 1 && b != 3) return 1;
+  memset(inv, 0, sizeof(double) * (size_t)(n_rows * b * b));
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const int64_t k = find_block(rp, ci, r, r);
+    double* out = inv + r * b * b;
+    if (k < 0) {
+      for (int i = 0; i < b; ++i) out[i * b + i] = 1.0;
+      continue;
+    }
+    const double* v = vals + k * b * b;
+    if (b == 1) {
+      const double d = v[0] + tau;
+      out[0] = (isfinite(d) && d != 0.0) ? 1.0 / d : 1.0;
+      continue;
+    }
+    double m[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) m[i * 3 + j] = v[i * 3 + j] + (i == j ? tau : 0.0);
+    const double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                       m[2] * (m[3] * m[7] - m[4] * m[6]);
+    if (!isfinite(det) || fabs(det) < 1e-300) {
+      for (int i = 0; i < 3; ++i) out[i * 3 + i] = 1.0;
+      continue;
+    }
+    const double id = 1.0 / det;
+    out[0] = (m[4] * m[8] - m[5] * m[7]) * id;
+    out[1] = (m[2] * m[7] - m[1] * m[8]) * id;
+    out[2] = (m[1] * m[5] - m[2] * m[4]) * id;
+    out[3] = (m[5] * m[6] - m[3] * m[8]) * id;
+    out[4] = (m[0] * m[8] - m[2] * m[6]) * id;
+    out[5] = (m[2] * m[3] - m[0] * m[5]) * id;
+    out[6] = (m[3] * m[7] - m[4] * m[6]) * id;
+    out[7] = (m[1] * m[6] - m[0] * m[7]) * id;
+    out[8] = (m[0] * m[4] - m[1] * m[3]) * id;
+  }
+  return 0;
+}
+
+static double sdot(const double* a, const double* b, int64_t n) {
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+  return acc;
+}
+
+static void block_apply(const double* blocks, int b, const double* x, double* y, int64_t n_rows) {
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const double* m = blocks + r * b * b;
+    for (int i = 0; i < b; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < b; ++j) acc += m[i * b + j] * x[r * b + j];
+      y[r * b + i] = acc;
+    }
+  }
+}
+
+/* pcg (optimizer.hpp:119-158): block-Jacobi PCG on (H + tau I) x = rhs from x = 0; stops on
+ * rel residual <= rel_tol (checked at the top of every iteration), non-positive curvature (at
+ * iteration 0 the preconditioned rhs is returned) or max_iters. */
+int oracle_pcg(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci, const double* vals, double tau,
+               const double* rhs, double* x, double rel_tol, int32_t max_iters, int32_t* iters,
+               int32_t* converged, int32_t* neg_curvature, double* rel_residual) {
+  const int64_t n = n_rows * b;
+  *iters = 0; *converged = 0; *neg_curvature = 0; *rel_residual = 0.0;
+  for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
+  const double rhs_norm = sqrt(sdot(rhs, rhs, n));
+  if (rhs_norm == 0.0) { *converged = 1; return 0; }
+  double* prec = malloc(sizeof(double) * (size_t)(n_rows * b * b));
+  double* r = malloc(sizeof(double) * (size_t)n);
+  double* z = malloc(sizeof(double) * (size_t)n);
+  double* p = malloc(sizeof(double) * (size_t)n);
+  double* q = malloc(sizeof(double) * (size_t)n);
+  oracle_block_jacobi_inverse(b, n_rows, rp, ci, vals, tau, prec);
+  memcpy(r, rhs, sizeof(double) * (size_t)n);
+  block_apply(prec, b, r, z, n_rows);
+  memcpy(p, z, sizeof(double) * (size_t)n);
+  double rz = sdot(r, z, n);
+  int done = 0;
+  for (int it = 0; it < max_iters && !done; ++it) {
+    const double rnorm = sqrt(sdot(r, r, n));
+    *rel_residual = rnorm / rhs_norm;
+    if (*rel_residual <= rel_tol) { *converged = 1; done = 1; break; }
+    oracle_bsr_matvec(b, n_rows, rp, ci, vals, p, q);
+    if (tau != 0.0)
+      for (int64_t i = 0; i < n; ++i) q[i] += tau * p[i];
+    const double pq = sdot(p, q, n);
+    if (!(pq > 0.0)) {
+      *neg_curvature = 1;
+      if (it == 0) memcpy(x, z, sizeof(double) * (size_t)n);
+      done = 1;
+      break;
+    }
+    const double alpha = rz / pq;
+    for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+    for (int64_t i = 0; i < n; ++i) r[i] -= alpha * q[i];
+    block_apply(prec, b, r, z, n_rows);
+    const double rz_next = sdot(r, z, n);
+    const double beta = rz_next / rz;
+    rz = rz_next;
+    for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    ++*iters;
+  }
+  if (!done) *rel_residual = sqrt(sdot(r, r, n)) / rhs_norm;
+  free(prec); free(r); free(z); free(p); free(q);
+  return 0;
+}

@@ -8,6 +8,9 @@
  *                            with gather_element_inputs  (registry.hpp:261-287) and
  *                            element_dofs                (registry.hpp:290-300)
  *   oracle_energy_only / oracle_guard_min <- assembly.hpp:131-173
+ *   oracle_bsr_matvec     <- BcrsMatrix::matvec          (assembly.hpp:43-57)
+ *   oracle_block_jacobi_inverse / oracle_pcg <- detail::block_jacobi_inverse, pcg
+ *                                               (optimizer.hpp:52-90, 119-158)
  * Pinned against the reference itself (oracle/_ref/ref_driver) by tests/test_oracle.py.
  */
 #ifndef SYMEL_ORACLE_H
@@ -62,4 +65,11 @@ int oracle_energy_only(const oracle_array* arrays, uint32_t n_arrays, const orac
 int oracle_guard_min(const oracle_array* arrays, uint32_t n_arrays, const oracle_energy* energies,
                      uint32_t n_energies, double* gmin);
 void oracle_free_result(oracle_result* res);
+int oracle_bsr_matvec(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci, const double* vals,
+                      const double* x, double* y);
+int oracle_block_jacobi_inverse(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci,
+                                const double* vals, double tau, double* inv);
+int oracle_pcg(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci, const double* vals, double tau,
+               const double* rhs, double* x, double rel_tol, int32_t max_iters, int32_t* iters,
+               int32_t* converged, int32_t* neg_curvature, double* rel_residual);
 #endif

@@ -140,6 +140,27 @@ int symel_cuda_copy_gradient(symel_cuda_ctx* ctx, double* host);
 int symel_cuda_copy_hessian(symel_cuda_ctx* ctx, double* host_values);
 int symel_cuda_device_results(symel_cuda_ctx* ctx, const double** grad, const double** values,
                               const int32_t** row_ptr, const int32_t** col_idx);
+/* ---- Consumer of the assembled Hessian (optimizer.hpp:52-158) -------------
+ * All act on the BCRS Hessian of the last successful assemble. Vectors have n_dofs entries;
+ * with SYMEL_PTR_DEVICE the pointers are device memory, otherwise host memory. */
+#define SYMEL_PTR_DEVICE 0x1u
+typedef struct {
+  int32_t iters;          /* PcgResult::iters */
+  int32_t converged;      /* PcgResult::converged */
+  int32_t neg_curvature;  /* PcgResult::neg_curvature */
+  int32_t reserved;
+  double rel_residual;    /* PcgResult::rel_residual */
+  double solve_ms;        /* device time of the solve (CUDA events) */
+} symel_cuda_pcg_result;
+/* y = H x (BcrsMatrix::matvec, assembly.hpp:43-57). */
+int symel_cuda_matvec(symel_cuda_ctx* ctx, const double* x, double* y, uint32_t flags);
+/* Inverses of the diagonal blocks + tau I, n_block_rows * b * b doubles, bit for bit as
+ * detail::block_jacobi_inverse (optimizer.hpp:52-90). */
+int symel_cuda_block_jacobi(symel_cuda_ctx* ctx, double tau, double* inv, uint32_t flags);
+/* pcg (optimizer.hpp:119-158): block-Jacobi PCG on (H + tau I) x = rhs from x = 0. */
+int symel_cuda_pcg(symel_cuda_ctx* ctx, double tau, const double* rhs, double* x, double rel_tol,
+                   int32_t max_iters, uint32_t flags, symel_cuda_pcg_result* res);
+
 /* Per-energy energy sums of the last assemble / energy_only (fixed-shape tree per energy; the
  * returned E is their sum in energy order). n must equal the number of energies. Used by the
  * sharded multi-GPU assembly, which all-reduces the part of the elements a rank owns. */

@@ -32,6 +32,7 @@
 #include "codegen.hpp"
 #include "factorize.hpp"
 #include "device_ops.hpp"
+#include "solver_ops.hpp"
 #include "sy_args.h"
 #include "tape_io.hpp"
 
@@ -186,6 +187,8 @@ struct symel_cuda_ctx {
   symel_cuda_timings timings{};
   std::uint64_t launches = 0;
   double last_E = 0.0;
+  bool assembled = false;      // d_vals / d_grad hold a completed assemble
+  dev::SolverWork solver;      // SpMV / PCG work vectors
 };
 
 namespace {
@@ -830,6 +833,7 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
 }
 
 double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st) {
+  c->assembled = false;
   prepare(c);
   refresh_activation(c);
   if (c->pattern_dirty) build_pattern(c);
@@ -981,7 +985,46 @@ double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st) {
     }
   }
   c->last_E = E;
+  c->assembled = true;
   return E;
+}
+
+// ------------------------------------------------------------- solver
+
+void free_solver(symel_cuda_ctx* c) {
+  dev::SolverWork& w = c->solver;
+  cfree(w.x); cfree(w.r); cfree(w.z); cfree(w.p); cfree(w.q); cfree(w.inv); cfree(w.partials);
+  cfree(w.ticket); cfree(w.sc);
+  w = dev::SolverWork{};
+}
+
+dev::SolverWork& ensure_solver(symel_cuda_ctx* c) {
+  if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+  if (!c->assembled) throw Fail{SYMEL_E_STATE, "solver: no assembled Hessian (call assemble first)"};
+  dev::SolverWork& w = c->solver;
+  if (w.n == c->n_dofs && w.x) return w;
+  free_solver(c);
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  const long long n = c->n_dofs;
+  w.vec_grid = (int)std::max<long long>(1, std::min<long long>((c->n_rows + 255) / 256, 8LL * nsm));
+  w.max_partials = (int)std::max<long long>(w.vec_grid, dev::spmv_partials_needed(c->b, c->n_rows));
+  dalloc(&w.x, n); dalloc(&w.r, n); dalloc(&w.z, n); dalloc(&w.p, n); dalloc(&w.q, n);
+  dalloc(&w.inv, (std::size_t)c->n_rows * c->b * c->b);
+  dalloc(&w.partials, 2 * (std::size_t)w.max_partials);
+  dalloc(&w.ticket, 1);
+  dalloc(&w.sc, 1);
+  CK(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned), c->stream));
+  w.n = n;
+  return w;
+}
+
+// A pointer argument of the solver calls: device memory (SYMEL_PTR_DEVICE) or host memory
+// staged through the given device buffer.
+const double* stage_in(symel_cuda_ctx* c, const double* p, double* dev_buf, std::uint32_t flags) {
+  if (flags & SYMEL_PTR_DEVICE) return p;
+  CK(cudaMemcpyAsync(dev_buf, p, sizeof(double) * c->n_dofs, cudaMemcpyHostToDevice, c->stream));
+  return dev_buf;
 }
 
 template <class F>
@@ -1055,6 +1098,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     if (c->refs_valid) dev::free_ordered_refs(&c->refs);
     if (c->tplan_valid) dev::free_tile_plan(&c->tplan);
     cfree(c->d_partials); cfree(c->d_gpartials); cfree(c->d_tileE);
+    free_solver(c);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     for (auto& kv : c->kcache)
       if (kv.second->lib) cudaLibraryUnload(kv.second->lib);
@@ -1363,6 +1407,83 @@ int symel_cuda_device_results(symel_cuda_ctx* c, const double** g, const double*
     if (v) *v = c->d_vals;
     if (rp) *rp = c->d_row_ptr;
     if (ci) *ci = c->d_col_idx;
+  });
+}
+
+int symel_cuda_matvec(symel_cuda_ctx* c, const double* x, double* y, uint32_t flags) {
+  return guarded(c, [&] {
+    dev::SolverWork& w = ensure_solver(c);
+    const double* xd = stage_in(c, x, w.p, flags);
+    double* yd = (flags & SYMEL_PTR_DEVICE) ? y : w.q;
+    CK(dev::bsr_spmv(c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, xd, yd, c->n_rows, 0.0, &w, nullptr, c->stream));
+    ++c->launches;
+    if (!(flags & SYMEL_PTR_DEVICE)) copy_sync(c, y, yd, sizeof(double) * c->n_dofs, cudaMemcpyDeviceToHost);
+    else CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_block_jacobi(symel_cuda_ctx* c, double tau, double* inv, uint32_t flags) {
+  return guarded(c, [&] {
+    dev::SolverWork& w = ensure_solver(c);
+    double* out = (flags & SYMEL_PTR_DEVICE) ? inv : w.inv;
+    CK(dev::block_jacobi_inverse(c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->n_rows, tau, out, c->stream));
+    ++c->launches;
+    const std::size_t bytes = sizeof(double) * (std::size_t)c->n_rows * c->b * c->b;
+    if (!(flags & SYMEL_PTR_DEVICE)) copy_sync(c, inv, out, bytes, cudaMemcpyDeviceToHost);
+    else CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_pcg(symel_cuda_ctx* c, double tau, const double* rhs, double* x, double rel_tol, int32_t max_iters,
+                   uint32_t flags, symel_cuda_pcg_result* res) {
+  return guarded(c, [&] {
+    if (!res) throw Fail{SYMEL_E_ARG, "pcg: result pointer is null"};
+    dev::SolverWork& w = ensure_solver(c);
+    *res = symel_cuda_pcg_result{};
+    cudaEventRecord(c->ev[0], c->stream);
+    const double* rd = stage_in(c, rhs, w.q, flags);  // q is free until the first iteration
+    CK(dev::block_jacobi_inverse(c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->n_rows, tau, w.inv, c->stream));
+    CK(dev::pcg_init(c->b, rd, &w, c->n_rows, c->stream));
+    c->launches += 2;
+    // rel_tol into the device scalars (staged through the pinned buffer, after the init kernel)
+    std::memcpy(c->h_pinned + 64, &rel_tol, sizeof(double));
+    CK(cudaMemcpyAsync(&w.sc->tol, c->h_pinned + 64, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    dev::PcgScalars h{};
+    auto fetch = [&] {
+      CK(cudaMemcpyAsync(c->h_pinned, w.sc, sizeof(dev::PcgScalars), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      std::memcpy(&h, c->h_pinned, sizeof h);
+    };
+    // Iterations are enqueued in batches; each one checks convergence on the device at its
+    // top and becomes a no-op once converged / negative curvature, so the host reads the
+    // scalars once per batch and the iteration semantics stay exactly optimizer.hpp:133-157.
+    constexpr int kBatch = 16;
+    int launched = 0;
+    fetch();
+    while (!h.done && launched < max_iters) {
+      const int nb = std::min(kBatch, max_iters - launched);
+      for (int k = 0; k < nb; ++k) {
+        CK(dev::pcg_iteration(c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, tau, &w, c->n_rows, launched + k,
+                              c->stream));
+        c->launches += 3;
+      }
+      launched += nb;
+      fetch();
+    }
+    res->iters = h.iters;
+    res->converged = h.converged;
+    res->neg_curvature = h.neg;
+    if (h.done) res->rel_residual = h.converged && h.rhs2 == 0.0 ? 0.0 : h.rel;
+    else res->rel_residual = std::sqrt(h.rr) / std::sqrt(h.rhs2);  // iterations exhausted
+    cudaEventRecord(c->ev[1], c->stream);
+    if (flags & SYMEL_PTR_DEVICE)
+      CK(cudaMemcpyAsync(x, w.x, sizeof(double) * c->n_dofs, cudaMemcpyDeviceToDevice, c->stream));
+    else
+      CK(cudaMemcpyAsync(x, w.x, sizeof(double) * c->n_dofs, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    res->solve_ms = ms;
   });
 }
 

@@ -60,6 +60,7 @@ EXPORTS = [
     "symel_cuda_assemble", "symel_cuda_energy_only", "symel_cuda_guard_min", "symel_cuda_pattern_info",
     "symel_cuda_copy_pattern", "symel_cuda_copy_gradient", "symel_cuda_copy_hessian",
     "symel_cuda_device_results", "symel_cuda_active_count", "symel_cuda_copy_active", "symel_cuda_energy_parts",
+    "symel_cuda_matvec", "symel_cuda_block_jacobi", "symel_cuda_pcg",
     "symel_cuda_element_outputs", "symel_cuda_get_timings", "symel_cuda_kernel_source",
     "symel_cuda_launch_count", "symel_cuda_fp64_peak", "symel_cuda_precompile", "symel_cuda_sync",
     "symel_cuda_stream", "symel_cuda_energy_info", "symel_cuda_plan_info",
@@ -110,6 +111,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "symel_cuda_device_results": ([P, P, P, P, P], I),
         "symel_cuda_active_count": ([P, I, C.POINTER(U64)], I),
         "symel_cuda_energy_parts": ([P, C.POINTER(C.c_double), C.c_uint32], I),
+        "symel_cuda_matvec": ([P, C.c_void_p, C.c_void_p, C.c_uint32], I),
+        "symel_cuda_block_jacobi": ([P, C.c_double, C.c_void_p, C.c_uint32], I),
+        "symel_cuda_pcg": ([P, C.c_double, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_uint32,
+                            C.POINTER(PcgResult)], I),
         "symel_cuda_copy_active": ([P, I, P], I),
         "symel_cuda_element_outputs": ([P, I, U64, U64, C.c_uint32, P], I),
         "symel_cuda_get_timings": ([P, C.POINTER(Timings)], I),
@@ -160,6 +165,15 @@ class Bcrs:
                 c = self.col_idx[k]
                 D[r * b:(r + 1) * b, c * b:(c + 1) * b] = v[k]
         return D
+
+
+class PcgResult(C.Structure):
+    """symel_cuda_pcg_result (PcgResult, optimizer.hpp:24-29, + device solve time)."""
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("neg_curvature", C.c_int32),
+                ("reserved", C.c_int32), ("rel_residual", C.c_double), ("solve_ms", C.c_double)]
+
+
+PTR_DEVICE = 1
 
 
 class DeviceAssembler:
@@ -304,6 +318,33 @@ class DeviceAssembler:
         v = np.empty(nb * b * b)
         self._check(self.lib.symel_cuda_copy_hessian(self.h, _ptr(v)))
         return v
+
+    # ---- consumer of the assembled Hessian --------------------------------
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        """y = H x with the last assembled Hessian (BcrsMatrix::matvec)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        self._check(self.lib.symel_cuda_matvec(self.h, x.ctypes.data, y.ctypes.data, 0))
+        return y
+
+    def block_jacobi(self, tau: float = 0.0) -> np.ndarray:
+        """Inverses of the diagonal blocks + tau I (detail::block_jacobi_inverse), [n_rows, b, b]."""
+        b, nbr, _, _ = self.pattern_info()
+        inv = np.empty(nbr * b * b)
+        self._check(self.lib.symel_cuda_block_jacobi(self.h, float(tau), inv.ctypes.data, 0))
+        return inv.reshape(nbr, b, b)
+
+    def pcg(self, rhs: np.ndarray, tau: float = 0.0, rel_tol: float = 1e-4, max_iters: int = 0):
+        """pcg (optimizer.hpp:119-158) on (H + tau I) x = rhs; max_iters <= 0 means n_dofs (the
+        Newton default, NewtonOptions::cg_max_iters). Returns (x, PcgResult as dict)."""
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty_like(rhs)
+        res = PcgResult()
+        mi = int(max_iters) if max_iters > 0 else rhs.size
+        self._check(self.lib.symel_cuda_pcg(self.h, float(tau), rhs.ctypes.data, x.ctypes.data, float(rel_tol), mi, 0,
+                                            C.byref(res)))
+        return x, {"iters": res.iters, "converged": bool(res.converged), "neg_curvature": bool(res.neg_curvature),
+                   "rel_residual": res.rel_residual, "solve_ms": res.solve_ms}
 
     def energy_parts(self) -> np.ndarray:
         """Per-energy energy sums of the last assemble / energy_only (energy registration order)."""

@@ -642,6 +642,13 @@ __global__ void k_tile_max(const int* __restrict__ tile_seg_ptr, const int* __re
   atomicMax(mx + 1, seg_con_ptr[s1] - seg_con_ptr[s0]);
 }
 
+// per segment: its first contribution relative to its tile's first (16 bits: <= 65535 per tile)
+__global__ void k_seg_rel(const int* __restrict__ seg_tile, const int* __restrict__ seg_con_ptr,
+                          const int* __restrict__ tile_con_ptr, long long n, unsigned short* __restrict__ rel) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rel[i] = (unsigned short)(seg_con_ptr[i] - tile_con_ptr[seg_tile[i]]);
+}
+
 __global__ void k_count_targets(const int* __restrict__ seg_target, long long n, int* __restrict__ count) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) atomicAdd(count + seg_target[i], 1);
@@ -776,6 +783,9 @@ int build_segments(unsigned long long* keys, unsigned short* vals, long long n, 
     sp->max_tile_seg = h[0];
     sp->max_tile_con = h[1];
     cudaFreeAsync(mx, S(s));
+    if (h[1] > 65535) return (int)cudaErrorInvalidValue;  // 16-bit relative contribution offsets
+    if ((err = tmp_alloc(&sp->seg_rel, nseg > 0 ? nseg : 1, s))) return err;
+    k_seg_rel<<<grid_for(nseg, 256), 256, 0, S(s)>>>(seg_tile, sp->seg_con_ptr, sp->tile_con_ptr, nseg, sp->seg_rel);
   }
   cudaFreeAsync(ukeys, S(s));
   cudaFreeAsync(counts, S(s));
@@ -987,7 +997,7 @@ int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_
 
 void free_tile_plan(TilePlan* p) {
   for (SegPlan* sp : {&p->h, &p->g})
-    for (void* q : {(void*)sp->tile_seg_ptr, (void*)sp->seg_target, (void*)sp->seg_con_ptr, (void*)sp->con,
+    for (void* q : {(void*)sp->tile_seg_ptr, (void*)sp->seg_target, (void*)sp->seg_con_ptr, (void*)sp->seg_rel, (void*)sp->con,
                     (void*)sp->seg_dst, (void*)sp->pt_ptr, (void*)sp->pt_target, (void*)sp->untouched,
                     (void*)sp->seg_mirror, (void*)sp->pt_mirror, (void*)sp->tile_con_ptr})
       if (q) cudaFree(q);

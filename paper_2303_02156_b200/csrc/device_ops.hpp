@@ -131,6 +131,7 @@ struct SegPlan {  // one of {Hessian blocks, gradient rows}
   int* seg_target = nullptr;    // block (or row) ordinal per segment
   int* seg_mirror = nullptr;    // Hessian: transposed block (== target on the diagonal)
   int* seg_con_ptr = nullptr;   // n_seg + 1
+  unsigned short* seg_rel = nullptr;  // n_seg: first contribution relative to its tile's
   unsigned short* con = nullptr;  // shared-memory offsets of the contributions (see TileSrc)
   int max_tile_seg = 0, max_tile_con = 0;  // per-tile maxima (shared-memory sizing)
   int* seg_dst = nullptr;       // >= 0 final target; < 0: -(partial index) - 1

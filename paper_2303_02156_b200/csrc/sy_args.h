@@ -25,14 +25,14 @@
     const int* tile_seg_ptr;                                                             \
     const int* tile_con_ptr;                                                             \
     const int* seg_block;                                                                \
-    const int* seg_con_ptr;                                                              \
+    const unsigned short* seg_rel;                                                       \
     const unsigned short* con;                                                           \
     const int* seg_dst;                                                                  \
     const int* seg_mirror;                                                               \
     const int* tile_gseg_ptr;                                                            \
     const int* tile_gcon_ptr;                                                            \
     const int* gseg_row;                                                                 \
-    const int* gseg_con_ptr;                                                             \
+    const unsigned short* gseg_rel;                                                      \
     const unsigned short* gcon;                                                          \
     const int* gseg_dst;                                                                 \
     int cap_hseg;                                                                        \

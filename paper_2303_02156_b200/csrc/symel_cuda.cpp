@@ -188,6 +188,11 @@ struct symel_cuda_ctx {
   std::uint64_t launches = 0;
   double last_E = 0.0;
   bool assembled = false;      // d_vals / d_grad hold a completed assemble
+  // energies' tile kernels run concurrently (their outputs are disjoint or fixed-order
+  // partials): fork from `stream` onto aux streams, join before the fix-up
+  static constexpr int kAux = 3;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kAux] = {};
   dev::SolverWork solver;      // SpMV / PCG work vectors
 };
 
@@ -427,7 +432,8 @@ Compiled* kernel_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   return e.k[v];
 }
 
-void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n, std::size_t smem = 0) {
+void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n, std::size_t smem = 0,
+            cudaStream_t stream = nullptr) {
   if (n <= 0) return;
   if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
   const long long blocks = (n - a.t0 + k->tpb - 1) / k->tpb;
@@ -437,7 +443,8 @@ void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n, std::size_t 
     k->smem_attr = smem;
   }
   void* params[] = {&a};
-  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, smem, c->stream));
+  CK(cudaLaunchKernel((const void*)k->kernel, dim3((unsigned)blocks), dim3((unsigned)k->tpb), params, smem,
+                      stream ? stream : c->stream));
   ++c->launches;
 }
 
@@ -739,8 +746,9 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
       mx[2] = std::max(mx[2], hc[t + 1] - hc[t]);
       mx[3] = std::max(mx[3], gc[t + 1] - gc[t]);
     }
-    e.cap[0] = mx[0] + 1;
-    e.cap[1] = mx[1] + 1;
+    // 32-bit words of the u16 slices (+1 for a slice starting at an odd index)
+    e.cap[0] = mx[0] / 2 + 2;
+    e.cap[1] = mx[1] / 2 + 2;
     e.cap[2] = mx[2] / 2 + 2;
     e.cap[3] = mx[3] / 2 + 2;
     cfree(e.d_gstage);
@@ -764,9 +772,22 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
     CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
   }
+  // energy kernels on separate streams (round robin over main + aux)
+  const bool concurrent = !std::getenv("SYMEL_SERIAL_ENERGIES");
+  bool aux_used[symel_cuda_ctx::kAux] = {};
+  int slot = 0;
+  if (concurrent) CK(cudaEventRecord(c->fork_ev, c->stream));
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
+    cudaStream_t est = c->stream;
+    if (concurrent && slot > 0) {
+      const int i = (slot - 1) % symel_cuda_ctx::kAux;
+      est = c->aux[i];
+      if (!aux_used[i]) CK(cudaStreamWaitEvent(est, c->fork_ev, 0));
+      aux_used[i] = true;
+    }
+    ++slot;
     const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
     Compiled* k = kernel_for(c, e, spd ? V_TILE_SPD : V_TILE);
     SyArgs a;
@@ -778,13 +799,13 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     a.bad_elem = c->d_bad + q;
     a.tile_seg_ptr = c->tplan.h.tile_seg_ptr;
     a.seg_block = c->tplan.h.seg_target;
-    a.seg_con_ptr = c->tplan.h.seg_con_ptr;
+    a.seg_rel = c->tplan.h.seg_rel;
     a.con = c->tplan.h.con;
     a.seg_dst = c->tplan.h.seg_dst;
     a.seg_mirror = c->tplan.h.seg_mirror;
     a.tile_gseg_ptr = c->tplan.g.tile_seg_ptr;
     a.gseg_row = c->tplan.g.seg_target;
-    a.gseg_con_ptr = c->tplan.g.seg_con_ptr;
+    a.gseg_rel = c->tplan.g.seg_rel;
     a.gcon = c->tplan.g.con;
     a.gseg_dst = c->tplan.g.seg_dst;
     a.partials = c->d_partials;
@@ -808,8 +829,13 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     }
     if (k->smem + plan_bytes > kTileSmemOne)
       throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': tile plan slice exceeds shared memory"};
-    launch(c, k, a, e.n_active, k->smem + plan_bytes);
+    launch(c, k, a, e.n_active, k->smem + plan_bytes, est);
   }
+  for (int i = 0; i < symel_cuda_ctx::kAux; ++i)
+    if (aux_used[i]) {
+      CK(cudaEventRecord(c->join_ev[i], c->aux[i]));
+      CK(cudaStreamWaitEvent(c->stream, c->join_ev[i], 0));
+    }
   cudaEventRecord(c->ev[1], c->stream);
   if (!atomic) {
     CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream));
@@ -868,9 +894,22 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
     CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
   }
+  // energy kernels on separate streams (round robin over main + aux)
+  const bool concurrent = !std::getenv("SYMEL_SERIAL_ENERGIES");
+  bool aux_used[symel_cuda_ctx::kAux] = {};
+  int slot = 0;
+  if (concurrent) CK(cudaEventRecord(c->fork_ev, c->stream));
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
+    cudaStream_t est = c->stream;
+    if (concurrent && slot > 0) {
+      const int i = (slot - 1) % symel_cuda_ctx::kAux;
+      est = c->aux[i];
+      if (!aux_used[i]) CK(cudaStreamWaitEvent(est, c->fork_ev, 0));
+      aux_used[i] = true;
+    }
+    ++slot;
     const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
     const bool staged = !atomic || spd;  // element outputs go through the contrib buffer
     ensure_elem_buffers(c, e, staged);
@@ -1077,6 +1116,9 @@ int symel_cuda_create(int device, symel_cuda_ctx** out) {
     if (cudaSetDevice(device) != cudaSuccess) return SYMEL_E_CUDA;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return SYMEL_E_CUDA;
     for (auto& ev : c->ev) cudaEventCreate(&ev);
+    for (auto& st : c->aux) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
+    for (auto& ev : c->join_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   }
   if (const char* d = std::getenv("SYMEL_CUDA_CACHE")) c->cache_dir = d;
   *out = c.release();
@@ -1103,6 +1145,9 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     for (auto& kv : c->kcache)
       if (kv.second->lib) cudaLibraryUnload(kv.second->lib);
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->join_ev) if (ev) cudaEventDestroy(ev);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    for (auto& st : c->aux) if (st) cudaStreamDestroy(st);
     cudaStreamDestroy(c->stream);
   }
   delete c;

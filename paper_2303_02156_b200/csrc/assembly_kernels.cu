@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include <limits>
 
@@ -642,6 +643,33 @@ __global__ void k_tile_max(const int* __restrict__ tile_seg_ptr, const int* __re
   atomicMax(mx + 1, seg_con_ptr[s1] - seg_con_ptr[s0]);
 }
 
+// segment sort key: tile-major, contribution count descending (stable: target order on ties)
+__global__ void k_seg_sort_keys(const unsigned long long* __restrict__ ukeys, const int* __restrict__ counts,
+                                long long n, unsigned long long* __restrict__ key, int* __restrict__ idx) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = ((ukeys[i] >> 32) << 32) | (unsigned long long)(0xffffffffu - (unsigned)counts[i]);
+  idx[i] = (int)i;
+}
+
+__global__ void k_seg_permute(const int* __restrict__ perm, const unsigned long long* __restrict__ ukeys,
+                              const int* __restrict__ counts, long long n, unsigned long long* __restrict__ ukeys2,
+                              int* __restrict__ counts2) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ukeys2[i] = ukeys[perm[i]];
+  counts2[i] = counts[perm[i]];
+}
+
+__global__ void k_con_permute(const int* __restrict__ perm, const int* __restrict__ old_ptr,
+                              const int* __restrict__ new_ptr, long long n, const unsigned short* __restrict__ con,
+                              unsigned short* __restrict__ con2) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int o = old_ptr[perm[i]], d = new_ptr[i], c = new_ptr[i + 1] - d;
+  for (int k = 0; k < c; ++k) con2[d + k] = con[o + k];
+}
+
 // per segment: its first contribution relative to its tile's first (16 bits: <= 65535 per tile)
 __global__ void k_seg_rel(const int* __restrict__ seg_tile, const int* __restrict__ seg_con_ptr,
                           const int* __restrict__ tile_con_ptr, long long n, unsigned short* __restrict__ rel) {
@@ -756,6 +784,41 @@ int build_segments(unsigned long long* keys, unsigned short* vals, long long n, 
     if (last == sentinel) --nseg;
   }
   sp->n_seg = nseg;
+  // Within each tile, order the segments by contribution count (descending, stable): the
+  // threads of a warp then reduce segments of similar length (less divergence). Tiles stay
+  // in order, so partials keep their (energy, tile) summation order.
+  if (nseg > 1 && !std::getenv("SYMEL_NO_SEG_SORT")) {
+    unsigned long long *skey, *skey2, *ukeys2;
+    int *sidx, *sidx2, *counts2, *old_ptr, *new_ptr;
+    unsigned short* con2;
+    if ((err = tmp_alloc(&skey, nseg, s)) || (err = tmp_alloc(&skey2, nseg, s)) || (err = tmp_alloc(&ukeys2, nseg, s)) ||
+        (err = tmp_alloc(&sidx, nseg, s)) || (err = tmp_alloc(&sidx2, nseg, s)) ||
+        (err = tmp_alloc(&counts2, nseg + 1, s)) || (err = tmp_alloc(&old_ptr, nseg + 1, s)) ||
+        (err = tmp_alloc(&new_ptr, nseg + 1, s)) || (err = tmp_alloc(&con2, n + 2, s)))
+      return err;
+    k_seg_sort_keys<<<grid_for(nseg, 256), 256, 0, S(s)>>>(ukeys, counts, nseg, skey, sidx);
+    tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, skey, skey2, sidx, sidx2, nseg, 0, end_bit, S(s));
+    if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+    cub::DeviceRadixSort::SortPairs(tmp, tb, skey, skey2, sidx, sidx2, nseg, 0, end_bit, S(s));
+    cudaFreeAsync(tmp, S(s));
+    k_seg_permute<<<grid_for(nseg, 256), 256, 0, S(s)>>>(sidx2, ukeys, counts, nseg, ukeys2, counts2);
+    cudaMemsetAsync(counts + nseg, 0, sizeof(int), S(s));
+    cudaMemsetAsync(counts2 + nseg, 0, sizeof(int), S(s));
+    tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, old_ptr, nseg + 1, S(s));
+    if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
+    cub::DeviceScan::ExclusiveSum(tmp, tb, counts, old_ptr, nseg + 1, S(s));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, counts2, new_ptr, nseg + 1, S(s));
+    cudaFreeAsync(tmp, S(s));
+    k_con_permute<<<grid_for(nseg, 256), 256, 0, S(s)>>>(sidx2, old_ptr, new_ptr, nseg, v2, con2);
+    cudaMemcpyAsync(ukeys, ukeys2, sizeof(unsigned long long) * nseg, cudaMemcpyDeviceToDevice, S(s));
+    cudaMemcpyAsync(counts, counts2, sizeof(int) * nseg, cudaMemcpyDeviceToDevice, S(s));
+    cudaMemcpyAsync(v2, con2, sizeof(unsigned short) * n, cudaMemcpyDeviceToDevice, S(s));
+    for (void* q : {(void*)skey, (void*)skey2, (void*)ukeys2, (void*)sidx, (void*)sidx2, (void*)counts2, (void*)old_ptr,
+                    (void*)new_ptr, (void*)con2})
+      cudaFreeAsync(q, S(s));
+  }
   // segment -> contribution ranges
   if ((err = tmp_alloc(&sp->seg_con_ptr, nseg + 1, s))) return err;
   cudaMemsetAsync(sp->seg_con_ptr + nseg, 0, sizeof(int), S(s));

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include <limits>
+#include <vector>
 
 #include "device_ops.hpp"
 
@@ -645,10 +646,12 @@ __global__ void k_tile_max(const int* __restrict__ tile_seg_ptr, const int* __re
 
 // segment sort key: tile-major, contribution count descending (stable: target order on ties)
 __global__ void k_seg_sort_keys(const unsigned long long* __restrict__ ukeys, const int* __restrict__ counts,
-                                long long n, unsigned long long* __restrict__ key, int* __restrict__ idx) {
+                                const unsigned char* __restrict__ tile_sort, long long n,
+                                unsigned long long* __restrict__ key, int* __restrict__ idx) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  key[i] = ((ukeys[i] >> 32) << 32) | (unsigned long long)(0xffffffffu - (unsigned)counts[i]);
+  const unsigned long long tile = ukeys[i] >> 32;
+  key[i] = (tile << 32) | (tile_sort[tile] ? (unsigned long long)(0xffffffffu - (unsigned)counts[i]) : 0ull);
   idx[i] = (int)i;
 }
 
@@ -749,7 +752,8 @@ unsigned long long key_sentinel(long long n_tiles) {
 }
 
 int build_segments(unsigned long long* keys, unsigned short* vals, long long n, long long n_tiles, long long n_targets,
-                   const int* row_ptr, const int* col_idx, long long n_rows, SegPlan* sp, void* s) {
+                   const int* row_ptr, const int* col_idx, long long n_rows, const unsigned char* tile_sort,
+                   SegPlan* sp, void* s) {
   int err;
   unsigned long long* k2;
   unsigned short* v2;
@@ -787,7 +791,7 @@ int build_segments(unsigned long long* keys, unsigned short* vals, long long n, 
   // Within each tile, order the segments by contribution count (descending, stable): the
   // threads of a warp then reduce segments of similar length (less divergence). Tiles stay
   // in order, so partials keep their (energy, tile) summation order.
-  if (nseg > 1 && !std::getenv("SYMEL_NO_SEG_SORT")) {
+  if (nseg > 1 && tile_sort && !std::getenv("SYMEL_NO_SEG_SORT")) {
     unsigned long long *skey, *skey2, *ukeys2;
     int *sidx, *sidx2, *counts2, *old_ptr, *new_ptr;
     unsigned short* con2;
@@ -796,7 +800,7 @@ int build_segments(unsigned long long* keys, unsigned short* vals, long long n, 
         (err = tmp_alloc(&counts2, nseg + 1, s)) || (err = tmp_alloc(&old_ptr, nseg + 1, s)) ||
         (err = tmp_alloc(&new_ptr, nseg + 1, s)) || (err = tmp_alloc(&con2, n + 2, s)))
       return err;
-    k_seg_sort_keys<<<grid_for(nseg, 256), 256, 0, S(s)>>>(ukeys, counts, nseg, skey, sidx);
+    k_seg_sort_keys<<<grid_for(nseg, 256), 256, 0, S(s)>>>(ukeys, counts, tile_sort, nseg, skey, sidx);
     tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, skey, skey2, sidx, sidx2, nseg, 0, end_bit, S(s));
     if ((err = tmp_alloc((char**)&tmp, tb, s))) return err;
@@ -1049,8 +1053,25 @@ int build_tile_plan(const TileSrc* src, int ne, long long n_blocks, long long n_
     ph += (unsigned long long)src[k].n_active * src[k].d.n_lb * src[k].d.n_lb;
     pg += (unsigned long long)src[k].n_active * src[k].d.n_lb;
   }
-  if ((err = build_segments(hk, hv, nh, tiles, n_blocks, row_ptr, col_idx, n_rows, &out->h, s))) return err;
-  if ((err = build_segments(gk, gv, ng, tiles, n_rows, nullptr, nullptr, 0, &out->g, s))) return err;
+  // per-tile segment-sort flags (energies staging in shared memory)
+  unsigned char* tsort = nullptr;
+  bool any_sort = false;
+  {
+    std::vector<unsigned char> h((size_t)(tiles > 0 ? tiles : 1), 0);
+    for (int k = 0; k < ne; ++k) {
+      const long long nt = (src[k].n_active + src[k].tpb - 1) / src[k].tpb;
+      for (long long t = 0; t < nt; ++t) h[(size_t)(src[k].tile_base + t)] = src[k].sort_segments ? 1 : 0;
+      any_sort = any_sort || (src[k].sort_segments && nt > 0);
+    }
+    if (any_sort) {
+      if ((err = tmp_alloc(&tsort, h.size(), s))) return err;
+      cudaMemcpyAsync(tsort, h.data(), h.size(), cudaMemcpyHostToDevice, S(s));
+      if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+    }
+  }
+  if ((err = build_segments(hk, hv, nh, tiles, n_blocks, row_ptr, col_idx, n_rows, tsort, &out->h, s))) return err;
+  if ((err = build_segments(gk, gv, ng, tiles, n_rows, nullptr, nullptr, 0, tsort, &out->g, s))) return err;
+  if (tsort) cudaFreeAsync(tsort, S(s));
   cudaFreeAsync(hk, S(s));
   cudaFreeAsync(hv, S(s));  // sorted copies live in SegPlan::con
   cudaFreeAsync(gk, S(s));

@@ -114,6 +114,7 @@ struct TileSrc {
   int tpb;
   int h0;            // first Hessian staging slot (1 + n_dofs); staging slot k of element tl
                      // lives at shared double k * tpb + tl (codegen.cpp tile layout)
+  int sort_segments; // order the tile's segments by contribution count (shared-memory staging)
   LbDesc d;
 };
 // A contribution is 16 bits (tpb = 128): Hessian (transpose << 15) | (sub(lo, hi) << 7) | tl,

@@ -702,6 +702,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     s.tpb = kTileElems;
     s.d = lb_desc(c, e);
     s.h0 = 1 + (int)e.dof_slots.size();
+    s.sort_segments = tile_global_stage(c, e) ? 0 : 1;  // L2-staged tiles keep target order
     // spatially coherent tiles: Morton order of element centroids (dof arrays as positions)
     dalloc(&e.d_tile_perm, (std::size_t)e.n_active);
     dalloc(&e.d_tile_elems, (std::size_t)e.n_active);

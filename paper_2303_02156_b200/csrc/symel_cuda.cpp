@@ -840,7 +840,8 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
   cudaEventRecord(c->ev[1], c->stream);
   if (!atomic) {
     CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream));
-    c->launches += 4;
+    c->launches += (c->tplan.h.n_pt > 0) + (c->tplan.g.n_pt > 0) + (c->tplan.h.n_untouched > 0) +
+                   (c->tplan.g.n_untouched > 0);
   }
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
@@ -1511,7 +1512,7 @@ int symel_cuda_pcg(symel_cuda_ctx* c, double tau, const double* rhs, double* x, 
       for (int k = 0; k < nb; ++k) {
         CK(dev::pcg_iteration(c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, tau, &w, c->n_rows, launched + k,
                               c->stream));
-        c->launches += 3;
+        c->launches += 4;  // SpMV, partial sum, update, direction
       }
       launched += nb;
       fetch();

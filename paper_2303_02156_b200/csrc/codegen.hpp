@@ -51,6 +51,9 @@ struct KernelSpec {
   bool fast = true;        // division strength reduction + FMA contraction
   std::uint32_t spd_m = 0; // fused_tile_spd: size m of the reduced eigenproblem
   bool stage_global = false;  // tile modes: stage element outputs in global memory (large elements)
+  int item_lanes = 1;         // tile mode with fixed summation: the n_items terms of an element
+                              // run on adjacent lanes (one term each) and are summed in order
+                              // with shuffles; elements per tile = threads_per_block / item_lanes
   bool plan_global = false;   // tile modes: read the plan slice from global memory (L2) instead of
                               // prefetching it to shared memory (keeps two CTAs per SM)
   int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)

@@ -64,6 +64,7 @@ struct Compiled {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   int tpb = 128;
+  int elems = 128;            // elements per CTA (tile kernels with item lanes: tpb / n_items)
   std::size_t smem = 0;       // dynamic shared memory per CTA (tile kernel: staging part)
   std::size_t smem_attr = 0;  // last MaxDynamicSharedMemorySize set on the kernel
   std::string source;
@@ -286,6 +287,7 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
   auto comp = std::make_unique<Compiled>();
   comp->source = std::move(src);
   comp->tpb = spec.threads_per_block;
+  comp->elems = spec.threads_per_block / std::max(1, spec.item_lanes);
   if (c->device >= 0) {
     CK(cudaLibraryLoadData(&comp->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CK(cudaLibraryGetKernel(&comp->kernel, comp->lib, spec.name.c_str()));
@@ -297,9 +299,18 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
 
 // Dynamic shared memory of the tile kernel: per element [E | g(n) | upper local-block
 // triangle of full b x b sub-blocks] (codegen.cpp stage layout), kTileElems elements.
+// Fixed-summation energies (n_items = 2, 4, 8: tet10's quadrature) run their item terms on
+// adjacent lanes in the tile kernel: 128 / n_items elements per tile.
+int tile_item_lanes(const Energy& e) {
+  if (std::getenv("SYMEL_NO_ITEM_LANES")) return 1;
+  const int n = (int)e.n_items;
+  return (n == 2 || n == 4 || n == 8) ? n : 1;
+}
+int tile_elems(const Energy& e) { return kTileElems / tile_item_lanes(e); }
+
 std::size_t tile_stage_doubles(const symel_cuda_ctx* c, const Energy& e) {
   const std::size_t n = e.dof_slots.size(), nlb = e.bm.n_lb, bb = std::size_t(c->b) * c->b;
-  return (1 + n + bb * nlb * (nlb + 1) / 2) * kTileElems;
+  return (1 + n + bb * nlb * (nlb + 1) / 2) * tile_elems(e);
 }
 // Elements whose staged outputs do not fit two CTAs per SM stage in global memory instead.
 bool tile_global_stage(const symel_cuda_ctx* c, const Energy& e) {
@@ -392,6 +403,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
     case V_TILE_G:
       s = base_spec(c, e, fast_tape(e));
       s.plan_global = v == V_TILE_G;
+      s.item_lanes = tile_item_lanes(e);
       s.mode = OutMode::fused_tile;
       s.schedule = -1;  // auto: lowest peak of live values
       s.threads_per_block = kTileElems;
@@ -436,7 +448,7 @@ void launch(symel_cuda_ctx* c, Compiled* k, SyArgs& a, long long n, std::size_t 
             cudaStream_t stream = nullptr) {
   if (n <= 0) return;
   if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
-  const long long blocks = (n - a.t0 + k->tpb - 1) / k->tpb;
+  const long long blocks = (n - a.t0 + k->elems - 1) / k->elems;
   if (!smem) smem = k->smem;
   if (smem > 48 * 1024 && smem != k->smem_attr) {
     CK(cudaKernelSetAttributeForDevice(k->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem, c->device));
@@ -699,7 +711,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     s.active = e.d_active;
     s.n_active = e.n_active;
     s.tile_base = tiles;
-    s.tpb = kTileElems;
+    s.tpb = tile_elems(e);
     s.d = lb_desc(c, e);
     s.h0 = 1 + (int)e.dof_slots.size();
     s.sort_segments = tile_global_stage(c, e) ? 0 : 1;  // L2-staged tiles keep target order
@@ -723,7 +735,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
       s.perm = nullptr;
     }
     src.push_back(s);
-    tiles += (e.n_active + kTileElems - 1) / kTileElems;
+    tiles += (e.n_active + tile_elems(e) - 1) / tile_elems(e);
   }
   CK(dev::build_tile_plan(src.data(), (int)src.size(), c->n_blocks, c->n_rows, c->d_row_ptr, c->d_col_idx, &c->tplan,
                           c->stream));
@@ -740,7 +752,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
   for (auto& ep : c->energies) {
     Energy& e = *ep;
     int mx[4] = {0, 0, 0, 0};
-    const long long nt = (e.skip || e.n_active == 0) ? 0 : (e.n_active + kTileElems - 1) / kTileElems;
+    const long long nt = (e.skip || e.n_active == 0) ? 0 : (e.n_active + tile_elems(e) - 1) / tile_elems(e);
     for (long long t = e.tile_base; t < e.tile_base + nt; ++t) {
       mx[0] = std::max(mx[0], hs[t + 1] - hs[t]);
       mx[1] = std::max(mx[1], gs[t + 1] - gs[t]);
@@ -846,7 +858,7 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    const long long nt = (e.n_active + kTileElems - 1) / kTileElems;
+    const long long nt = (e.n_active + tile_elems(e) - 1) / tile_elems(e);
     ensure_elem_buffers(c, e, false);
     CK(dev::tile_energy(c->d_tileE, e.tile_base, nt, c->d_partial, c->d_energy + q, c->stream));
     c->launches += 2;

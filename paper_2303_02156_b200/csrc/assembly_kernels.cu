@@ -1102,6 +1102,19 @@ int tile_fixup(const TilePlan& p, const double* partials, const double* gpartial
   return (int)cudaGetLastError();
 }
 
+__global__ void k_soa_gather(const double* __restrict__ src, int comps, const int* __restrict__ map, long long n,
+                             long long stride, double* __restrict__ dst) {
+  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const long long el = map ? (long long)map[pos] : pos;
+  for (int c = 0; c < comps; ++c) dst[(long long)c * stride + pos] = src[el * comps + c];
+}
+
+int soa_gather(const double* src, int comps, const int* map, long long n, long long stride, double* dst, void* s) {
+  if (n > 0) k_soa_gather<<<grid_for(n, 256), 256, 0, S(s)>>>(src, comps, map, n, stride, dst);
+  return (int)cudaGetLastError();
+}
+
 int tile_energy(const double* tileE, long long first, long long n, double* partial, double* out, void* s) {
   return energy_tree(tileE + first, 1, n, partial, out, s);
 }

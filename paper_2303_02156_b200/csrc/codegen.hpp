@@ -54,6 +54,8 @@ struct KernelSpec {
   int item_lanes = 1;         // tile mode with fixed summation: the n_items terms of an element
                               // run on adjacent lanes (one term each) and are summed in order
                               // with shuffles; elements per tile = threads_per_block / item_lanes
+  std::vector<std::uint8_t> soa_arrays;  // tile modes: per array, 1 = elem_comp inputs read
+                                         // from a tile-ordered SoA copy a.arr[i][c * soa_n + t]
   bool plan_global = false;   // tile modes: read the plan slice from global memory (L2) instead of
                               // prefetching it to shared memory (keeps two CTAs per SM)
   int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)

@@ -151,6 +151,10 @@ void free_tile_plan(TilePlan* p);
 // vals/grad for partial targets and untouched targets; deterministic (fixed order)
 int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals,
                double* grad, void* stream);
+// Tile-ordered SoA copy of a per-element array: dst[c * stride + pos] = src[elem(pos) * comps + c],
+// elem(pos) = map[pos] (map == nullptr: identity), pos < n.
+int soa_gather(const double* src, int comps, const int* map, long long n, long long stride, double* dst,
+               void* stream);
 // fixed-order sum of per-tile energies [first, first + n) into *out
 int tile_energy(const double* tileE, long long first, long long n, double* partial, double* out, void* stream);
 

@@ -45,6 +45,7 @@
     double* gstage;                                                                      \
     long long tile_base;                                                                 \
     int tile_atomic;                                                                     \
+    long long soa_n;                                                                     \
     double params[32];                                                                   \
   };
 

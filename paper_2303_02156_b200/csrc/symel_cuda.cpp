@@ -99,6 +99,8 @@ struct Array {
   std::uint32_t comps = 0;
   bool is_dof = false;
   double* d = nullptr;
+  std::uint64_t version = 0;  // bumped by every set_array (SoA copies are rebuilt from it)
+  bool external = false;      // device pointer handed out: treat as changed every assemble
 };
 
 struct Conn {
@@ -146,6 +148,11 @@ struct Energy {
   int* d_tile_elems = nullptr; // tile position -> element id
   int cap[4] = {0, 0, 0, 0};   // shared plan-slice capacities (words): hseg, gseg, hcon, gcon
   double* d_gstage = nullptr;  // global staging (large elements): one slab per tile
+  // tile-ordered SoA copies of wide per-element arrays (elem_comp inputs): array -> copy
+  std::map<int, double*> d_soa;
+  std::map<int, std::uint64_t> soa_version;
+  long long soa_n = 0;          // SoA stride (n_active of the plan they were built for)
+  std::uint64_t soa_epoch = ~0ull;
 };
 
 }  // namespace
@@ -174,6 +181,7 @@ struct symel_cuda_ctx {
   bool refs_valid = false;
   dev::TilePlan tplan;
   bool tplan_valid = false;
+  std::uint64_t plan_epoch = 0;  // bumped on every tile-plan build (tile order may change)
   double* d_partials = nullptr;
   double* d_gpartials = nullptr;
   double* d_tileE = nullptr;
@@ -358,6 +366,41 @@ KernelSpec base_spec(symel_cuda_ctx* c, const Energy& e, const TapeIR* tape) {
   return s;
 }
 
+// Wide per-element arrays (elem_comp inputs, >= 4 components) are read by the tile kernels from
+// a tile-ordered SoA copy: the threads of a warp (consecutive tile positions) read consecutive
+// doubles instead of one strided row each (the 144-double bending Q, pair offsets, rest frames).
+constexpr std::uint32_t kSoaMinComps = 4;
+std::vector<std::uint8_t> soa_arrays_of(const symel_cuda_ctx* c, const Energy& e) {
+  std::vector<std::uint8_t> v(c->arrays.size(), 0);
+  if (std::getenv("SYMEL_NO_SOA")) return v;
+  for (const InputBinding& in : e.inputs)
+    if (in.kind == InKind::elem_comp && c->arrays[in.array].comps >= kSoaMinComps) v[in.array] = 1;
+  return v;
+}
+
+void ensure_soa(symel_cuda_ctx* c, Energy& e) {
+  const std::vector<std::uint8_t> soa = soa_arrays_of(c, e);
+  const int* map = e.d_tile_perm ? e.d_tile_elems : e.d_active;
+  for (std::size_t i = 0; i < soa.size(); ++i) {
+    if (!soa[i]) continue;
+    const Array& arr = c->arrays[i];
+    double*& buf = e.d_soa[(int)i];
+    const bool fresh = buf && e.soa_n == e.n_active && e.soa_epoch == c->plan_epoch &&
+                       e.soa_version[(int)i] == arr.version && !arr.external;
+    if (fresh) continue;
+    if (!buf || e.soa_n != e.n_active) {
+      cfree(buf);
+      buf = nullptr;
+      dalloc(&buf, (std::size_t)arr.comps * std::max<long long>(1, e.n_active));
+    }
+    CK(dev::soa_gather(arr.d, (int)arr.comps, map, e.n_active, e.n_active, buf, c->stream));
+    ++c->launches;
+    e.soa_version[(int)i] = arr.version;
+  }
+  e.soa_n = e.n_active;
+  e.soa_epoch = c->plan_epoch;
+}
+
 KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
   KernelSpec s;
   switch (v) {
@@ -404,6 +447,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s = base_spec(c, e, fast_tape(e));
       s.plan_global = v == V_TILE_G;
       s.item_lanes = tile_item_lanes(e);
+      s.soa_arrays = soa_arrays_of(c, e);
       s.mode = OutMode::fused_tile;
       s.schedule = -1;  // auto: lowest peak of live values
       s.threads_per_block = kTileElems;
@@ -416,6 +460,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       if (!tp) throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': no reduced SPD form"};
       s = base_spec(c, e, tp);
       s.plan_global = v == V_TILE_SPD_G;
+      s.soa_arrays = soa_arrays_of(c, e);
       s.mode = OutMode::fused_tile_spd;
       s.spd_m = e.spd_info.frontier;
       s.schedule = -1;
@@ -769,6 +814,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     if (nt > 0 && tile_global_stage(c, e)) dalloc(&e.d_gstage, (std::size_t)nt * tile_stage_doubles(c, e));
   }
   c->tplan_valid = true;
+  ++c->plan_epoch;
   cudaEventRecord(c->ev[1], c->stream);
   cudaEventSynchronize(c->ev[1]);
   float ms = 0;
@@ -806,6 +852,9 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     SyArgs a;
     fill_args(c, e, a);
     a.active = e.d_tile_perm ? e.d_tile_elems : e.d_active;  // elements in tile order
+    ensure_soa(c, e);
+    for (const auto& kv : e.d_soa) a.arr[kv.first] = kv.second;
+    a.soa_n = e.soa_n;
     a.n = e.n_active;
     a.grad = c->d_grad;
     a.vals = c->d_vals;
@@ -1148,6 +1197,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     for (auto& e : c->energies) {
       cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
       cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems); cfree(e->d_gstage);
+      for (auto& kv : e->d_soa) cfree(kv.second);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
     cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
@@ -1208,6 +1258,7 @@ int symel_cuda_set_array(symel_cuda_ctx* c, int id, const double* host, uint64_t
     if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
     CK(cudaMemcpyAsync(a.d, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    ++a.version;
   });
 }
 
@@ -1222,7 +1273,11 @@ int symel_cuda_get_array(symel_cuda_ctx* c, int id, double* host, uint64_t count
 }
 
 int symel_cuda_array_device_ptr(symel_cuda_ctx* c, int id, double** p) {
-  return guarded(c, [&] { *p = array_of(c, id).d; });
+  return guarded(c, [&] {
+    Array& a = array_of(c, id);
+    a.external = true;  // may be written behind our back: SoA copies refresh every assemble
+    *p = a.d;
+  });
 }
 
 int symel_cuda_add_connectivity(symel_cuda_ctx* c, const char* name, uint32_t arity, int* id) {

@@ -229,7 +229,7 @@ def main():
     from paper_2303_02156_b200.parallel import ShardedTetSystem, max_over_ranks, sum_over_ranks
     from paper_2303_02156_b200.systems import DeviceSystem
 
-    if world > 1 and args.config == "c2":
+    if (world > 1 or os.environ.get("BENCH_FORCE_SLABS")) and args.config == "c2":
         # sharded, weak scaling: rank r owns a config-2-sized slab (100 x 100 x 100 hexes) of a
         # world*100 x 100 x 100 grid plus one ghost hex plane; the data-path collective is the
         # all-reduce of the owned energy (parallel.py)

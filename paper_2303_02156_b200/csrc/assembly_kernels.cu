@@ -730,10 +730,19 @@ __global__ void k_fixup(const int* __restrict__ pt_ptr, const int* __restrict__ 
   if (q >= n_pt * w) return;
   const long long p = q / w;
   const int ent = (int)(q % w);
+  const int k0 = __ldg(pt_ptr + p), k1 = __ldg(pt_ptr + p + 1);
+  const int tg = __ldg(pt_target + p), mr = mirror ? __ldg(mirror + p) : tg;
+  // partials in slot order; four loads in flight per step (same left-to-right sum)
   double acc = 0.0;
-  for (int k = pt_ptr[p]; k < pt_ptr[p + 1]; ++k) acc += partials[(long long)k * w + ent];
-  out[(long long)pt_target[p] * w + ent] = acc;
-  if (mirror && mirror[p] != pt_target[p]) out[(long long)mirror[p] * w + (ent % b) * b + ent / b] = acc;
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    const double v0 = __ldcs(partials + (long long)k * w + ent), v1 = __ldcs(partials + (long long)(k + 1) * w + ent);
+    const double v2 = __ldcs(partials + (long long)(k + 2) * w + ent), v3 = __ldcs(partials + (long long)(k + 3) * w + ent);
+    acc = (((acc + v0) + v1) + v2) + v3;
+  }
+  for (; k < k1; ++k) acc += __ldcs(partials + (long long)k * w + ent);
+  out[(long long)tg * w + ent] = acc;
+  if (mr != tg) out[(long long)mr * w + (ent % b) * b + ent / b] = acc;
 }
 
 __global__ void k_zero_targets(const int* __restrict__ tg, long long n, int w, double* __restrict__ out) {

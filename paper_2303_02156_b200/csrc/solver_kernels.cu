@@ -3,8 +3,9 @@
 // (/root/reference/proj/include/symel/assembly.hpp:43-57, optimizer.hpp:52-158).
 //
 // The SpMV is HBM-bound (72 B of block values + 4 B of column index per 3x3 block, x gathers
-// hit L2): G lanes per block row, each lane walks the row's blocks with stride G (consecutive
-// lanes read consecutive blocks), then a fixed xor-shuffle tree sums the G partial rows.
+// hit L2): G = 8 lanes per block row, each lane walks the row's blocks with stride G
+// (consecutive lanes read consecutive blocks), then a fixed xor-shuffle tree sums the G
+// partial rows.
 // Dot products are deterministic: per-CTA partials in a fixed grid, summed in CTA order by the
 // last CTA to finish (ticket counter), so results do not depend on scheduling. The
 // block-Jacobi inverse reproduces the reference's adjugate formula bit for bit (no
@@ -12,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "solver_ops.hpp"
 
@@ -316,12 +318,14 @@ int grid_rows(long long n_rows, int rows_per_cta) {
 int bsr_spmv(int b, const int* row_ptr, const int* col_idx, const double* vals, const double* x, double* y,
              long long n_rows, double tau, SolverWork* w, double* dot_out, void* stream, PcgScalars* pcg) {
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = grid_rows(n_rows, kThreads / (b == 3 ? 16 : 8));
+  // b = 3: 8 lanes per block row (config 2: 15 blocks per row, ~2 per lane); measured on B200
+  // 4 / 8 / 16 / 32 lanes: 72 / 83 / 75 / 50 % of the HBM roofline
+  constexpr int G3 = 8;
+  const int grid = grid_rows(n_rows, kThreads / (b == 3 ? G3 : 8));
   if (dot_out && grid > w->max_partials) return (int)cudaErrorInvalidValue;
   if (b == 3) {
-    constexpr int G = 16;
-    k_spmv<3, G><<<grid, kThreads, 0, s>>>(row_ptr, col_idx, vals, x, y, n_rows, tau, w->partials, w->ticket, dot_out,
-                                           pcg);
+    k_spmv<3, G3><<<grid, kThreads, 0, s>>>(row_ptr, col_idx, vals, x, y, n_rows, tau, w->partials, w->ticket, dot_out,
+                                            pcg);
   } else if (b == 1) {
     constexpr int G = 8;
     k_spmv<1, G><<<grid, kThreads, 0, s>>>(row_ptr, col_idx, vals, x, y, n_rows, tau, w->partials, w->ticket, dot_out,
@@ -334,7 +338,7 @@ int bsr_spmv(int b, const int* row_ptr, const int* col_idx, const double* vals, 
 }
 
 long long spmv_partials_needed(int b, long long n_rows) {
-  return grid_rows(n_rows, kThreads / (b == 3 ? 16 : 8));
+  return grid_rows(n_rows, kThreads / 8);
 }
 
 int block_jacobi_inverse(int b, const int* row_ptr, const int* col_idx, const double* vals, long long n_rows,

@@ -957,22 +957,9 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
     CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
   }
-  // energy kernels on separate streams (round robin over main + aux)
-  const bool concurrent = !std::getenv("SYMEL_SERIAL_ENERGIES");
-  bool aux_used[symel_cuda_ctx::kAux] = {};
-  int slot = 0;
-  if (concurrent) CK(cudaEventRecord(c->fork_ev, c->stream));
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    cudaStream_t est = c->stream;
-    if (concurrent && slot > 0) {
-      const int i = (slot - 1) % symel_cuda_ctx::kAux;
-      est = c->aux[i];
-      if (!aux_used[i]) CK(cudaStreamWaitEvent(est, c->fork_ev, 0));
-      aux_used[i] = true;
-    }
-    ++slot;
     const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
     const bool staged = !atomic || spd;  // element outputs go through the contrib buffer
     ensure_elem_buffers(c, e, staged);

@@ -161,6 +161,11 @@ int symel_cuda_block_jacobi(symel_cuda_ctx* ctx, double tau, double* inv, uint32
 int symel_cuda_pcg(symel_cuda_ctx* ctx, double tau, const double* rhs, double* x, double rel_tol,
                    int32_t max_iters, uint32_t flags, symel_cuda_pcg_result* res);
 
+/* The flat dof vector (n_dofs doubles, dof arrays in registration order): EnergySystem::
+ * gather_dofs / scatter_dofs (registry.hpp:220-238), for a Newton loop on the device. */
+int symel_cuda_gather_dofs(symel_cuda_ctx* ctx, double* u, uint32_t flags);
+int symel_cuda_scatter_dofs(symel_cuda_ctx* ctx, const double* u, uint32_t flags);
+
 /* Per-energy energy sums of the last assemble / energy_only (fixed-shape tree per energy; the
  * returned E is their sum in energy order). n must equal the number of energies. Used by the
  * sharded multi-GPU assembly, which all-reduces the part of the elements a rank owns. */

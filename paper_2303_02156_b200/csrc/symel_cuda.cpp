@@ -1470,6 +1470,7 @@ int symel_cuda_guard_min(symel_cuda_ctx* c, double* gmin) {
 
 int symel_cuda_pattern_info(symel_cuda_ctx* c, int* b, uint64_t* nbr, uint64_t* nb, uint64_t* nd) {
   return guarded(c, [&] {
+    if (c->topology_dirty) refresh_layout(c);  // b, rows and dofs are known before the first assemble
     if (b) *b = c->b;
     if (nbr) *nbr = (uint64_t)c->n_rows;
     if (nb) *nb = (uint64_t)c->n_blocks;
@@ -1585,6 +1586,36 @@ int symel_cuda_pcg(symel_cuda_ctx* c, double tau, const double* rhs, double* x, 
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     res->solve_ms = ms;
+  });
+}
+
+// EnergySystem::gather_dofs / scatter_dofs (registry.hpp:220-238): the flat dof vector in
+// layout order (dof arrays in registration order, each items * comps).
+int symel_cuda_gather_dofs(symel_cuda_ctx* c, double* u, uint32_t flags) {
+  return guarded(c, [&] {
+    if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+    if (c->topology_dirty) refresh_layout(c);
+    const cudaMemcpyKind kind = (flags & SYMEL_PTR_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    for (std::size_t i = 0; i < c->arrays.size(); ++i)
+      if (c->set_off[i] >= 0)
+        CK(cudaMemcpyAsync(u + c->set_off[i], c->arrays[i].d, sizeof(double) * c->arrays[i].items * c->arrays[i].comps,
+                           kind, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int symel_cuda_scatter_dofs(symel_cuda_ctx* c, const double* u, uint32_t flags) {
+  return guarded(c, [&] {
+    if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
+    if (c->topology_dirty) refresh_layout(c);
+    const cudaMemcpyKind kind = (flags & SYMEL_PTR_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (std::size_t i = 0; i < c->arrays.size(); ++i)
+      if (c->set_off[i] >= 0) {
+        Array& a = c->arrays[i];
+        CK(cudaMemcpyAsync(a.d, u + c->set_off[i], sizeof(double) * a.items * a.comps, kind, c->stream));
+        ++a.version;
+      }
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -60,7 +60,8 @@ EXPORTS = [
     "symel_cuda_assemble", "symel_cuda_energy_only", "symel_cuda_guard_min", "symel_cuda_pattern_info",
     "symel_cuda_copy_pattern", "symel_cuda_copy_gradient", "symel_cuda_copy_hessian",
     "symel_cuda_device_results", "symel_cuda_active_count", "symel_cuda_copy_active", "symel_cuda_energy_parts",
-    "symel_cuda_matvec", "symel_cuda_block_jacobi", "symel_cuda_pcg",
+    "symel_cuda_matvec", "symel_cuda_block_jacobi", "symel_cuda_pcg", "symel_cuda_gather_dofs",
+    "symel_cuda_scatter_dofs",
     "symel_cuda_element_outputs", "symel_cuda_get_timings", "symel_cuda_kernel_source",
     "symel_cuda_launch_count", "symel_cuda_fp64_peak", "symel_cuda_precompile", "symel_cuda_sync",
     "symel_cuda_stream", "symel_cuda_energy_info", "symel_cuda_plan_info",
@@ -112,6 +113,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "symel_cuda_active_count": ([P, I, C.POINTER(U64)], I),
         "symel_cuda_energy_parts": ([P, C.POINTER(C.c_double), C.c_uint32], I),
         "symel_cuda_matvec": ([P, C.c_void_p, C.c_void_p, C.c_uint32], I),
+        "symel_cuda_gather_dofs": ([P, C.c_void_p, C.c_uint32], I),
+        "symel_cuda_scatter_dofs": ([P, C.c_void_p, C.c_uint32], I),
         "symel_cuda_block_jacobi": ([P, C.c_double, C.c_void_p, C.c_uint32], I),
         "symel_cuda_pcg": ([P, C.c_double, C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_uint32,
                             C.POINTER(PcgResult)], I),
@@ -345,6 +348,18 @@ class DeviceAssembler:
                                             C.byref(res)))
         return x, {"iters": res.iters, "converged": bool(res.converged), "neg_curvature": bool(res.neg_curvature),
                    "rel_residual": res.rel_residual, "solve_ms": res.solve_ms}
+
+    def gather_dofs(self) -> np.ndarray:
+        """EnergySystem::gather_dofs: the flat dof vector (dof arrays in registration order)."""
+        _, _, _, nd = self.pattern_info()
+        u = np.empty(nd)
+        self._check(self.lib.symel_cuda_gather_dofs(self.h, u.ctypes.data, 0))
+        return u
+
+    def scatter_dofs(self, u: np.ndarray) -> None:
+        """EnergySystem::scatter_dofs."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        self._check(self.lib.symel_cuda_scatter_dofs(self.h, u.ctypes.data, 0))
 
     def energy_parts(self) -> np.ndarray:
         """Per-energy energy sums of the last assemble / energy_only (energy registration order)."""

@@ -76,3 +76,18 @@ def test_pcg(assembled, oracle_mod, tol):
                 assert np.abs(x - xr).max() / max(1e-300, np.abs(xr).max()) <= 1e-8
         x2, st2 = ds.asm.pcg(-g, tau, tol, n)
         assert np.array_equal(x, x2) and st2["iters"] == st["iters"]
+
+
+def test_gather_scatter_dofs():
+    """EnergySystem::gather_dofs / scatter_dofs (registry.hpp:220-238) on the device arrays."""
+    case = C.config2(5)
+    ds = DeviceSystem(case)
+    u = ds.asm.gather_dofs()
+    assert np.array_equal(u, case.x.ravel())
+    u2 = u + 1e-4 * np.sin(np.arange(u.size))
+    ds.asm.scatter_dofs(u2)
+    assert np.array_equal(ds.asm.gather_dofs(), u2)
+    E = ds.asm.assemble("deterministic")
+    moved = C.Case(case.name, case.kind, u2.reshape(-1, 3), case.X, case.conn, case.params)
+    E2 = DeviceSystem(moved).asm.assemble("deterministic")
+    assert E == E2

@@ -59,7 +59,7 @@ def test_row_windows_match_oracle(name, oracle_mod):
     n = case.n_nodes
     # c5's window oracle also runs the whole inertia energy and the contact tape in IEEE
     # mode: smaller windows keep the test in seconds
-    for frac in ((0.0, 0.5) if case.kind == "contact" else (0.0, 0.37, 0.93)):
+    for frac in ((0.0, 0.5) if case.kind in ("contact", "tet4") else (0.0, 0.37, 0.93)):
         lo = int(frac * n)
         hi = min(n, lo + max(64, n // (1000 if case.kind == "contact" else 200)))
         sysm = oracle_mod.system_for_case(window_case(case, lo, hi), golden_tape)
@@ -90,9 +90,11 @@ def test_full_system_properties(name):
     pos = np.searchsorted(key, tkey)
     assert np.array_equal(key[pos], tkey)
     assert np.array_equal(np.unique(rows[rows == cols]), np.arange(H.n_block_rows))
-    # values: every block is the exact transpose of its mirror
+    # values: every block is the exact transpose of its mirror (a seeded sample of 2 M blocks
+    # on the largest system)
     v = H.values.reshape(nb, b, b)
-    assert np.array_equal(v, np.swapaxes(v[pos], 1, 2))
+    pick = np.arange(nb) if nb <= 2_000_000 else np.random.default_rng(5).choice(nb, 2_000_000, replace=False)
+    assert np.array_equal(v[pick], np.swapaxes(v[pos[pick]], 1, 2))
     # deterministic vs atomic
     Ea = ds.asm.assemble("atomic")
     assert abs(Ea - E) <= 1e-12 * max(1.0, abs(E))

@@ -124,7 +124,10 @@ int symel_cuda_set_pins(symel_cuda_ctx* ctx, const uint8_t* mask, uint64_t n_dof
 /* Refreshes activation, (re)builds the pattern when topology or activation changed,
  * evaluates every active element, assembles g and the BCRS values on the device and
  * returns E. On a non-finite output returns SYMEL_E_NONFINITE with *status naming the first
- * (energy, element), like check_finite. */
+ * (energy, element), like check_finite. Deterministic mode returns as soon as E and the
+ * gradient are final; the Hessian fix-up may still run on the context stream, and every call
+ * of this API that reads the matrix is ordered after it (raw device_results pointers: call
+ * symel_cuda_sync first). */
 int symel_cuda_assemble(symel_cuda_ctx* ctx, uint32_t flags, double* energy, symel_cuda_status* status);
 /* Energy over the currently active elements; non-finite values are returned, not raised. */
 int symel_cuda_energy_only(symel_cuda_ctx* ctx, double* energy);

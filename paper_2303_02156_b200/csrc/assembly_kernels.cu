@@ -1098,16 +1098,22 @@ void free_tile_plan(TilePlan* p) {
 }
 
 int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals, double* grad,
-               void* s) {
+               void* s, int which) {
   const int bb = b * b;
+  if (which & 1) {
   if (p.h.n_pt)
     k_fixup<<<grid_for(p.h.n_pt * bb, 256), 256, 0, S(s)>>>(p.h.pt_ptr, p.h.pt_target, p.h.pt_mirror, p.h.n_pt, bb, b,
                                                             partials, vals);
-  if (p.g.n_pt)
-    k_fixup<<<grid_for(p.g.n_pt * b, 256), 256, 0, S(s)>>>(p.g.pt_ptr, p.g.pt_target, nullptr, p.g.n_pt, b, b,
-                                                           gpartials, grad);
-  if (p.h.n_untouched) k_zero_targets<<<grid_for(p.h.n_untouched * bb, 256), 256, 0, S(s)>>>(p.h.untouched, p.h.n_untouched, bb, vals);
-  if (p.g.n_untouched) k_zero_targets<<<grid_for(p.g.n_untouched * b, 256), 256, 0, S(s)>>>(p.g.untouched, p.g.n_untouched, b, grad);
+    if (p.h.n_untouched)
+      k_zero_targets<<<grid_for(p.h.n_untouched * bb, 256), 256, 0, S(s)>>>(p.h.untouched, p.h.n_untouched, bb, vals);
+  }
+  if (which & 2) {
+    if (p.g.n_pt)
+      k_fixup<<<grid_for(p.g.n_pt * b, 256), 256, 0, S(s)>>>(p.g.pt_ptr, p.g.pt_target, nullptr, p.g.n_pt, b, b,
+                                                             gpartials, grad);
+    if (p.g.n_untouched)
+      k_zero_targets<<<grid_for(p.g.n_untouched * b, 256), 256, 0, S(s)>>>(p.g.untouched, p.g.n_untouched, b, grad);
+  }
   return (int)cudaGetLastError();
 }
 

@@ -149,8 +149,9 @@ int build_tile_plan(const TileSrc* src, int n_energies, long long n_blocks, long
                     const int* col_idx, TilePlan* out, void* stream);
 void free_tile_plan(TilePlan* p);
 // vals/grad for partial targets and untouched targets; deterministic (fixed order)
+// which: 1 = Hessian targets, 2 = gradient rows, 3 = both
 int tile_fixup(const TilePlan& p, const double* partials, const double* gpartials, int b, double* vals,
-               double* grad, void* stream);
+               double* grad, void* stream, int which = 3);
 // Tile-ordered SoA copy of a per-element array: dst[c * stride + pos] = src[elem(pos) * comps + c],
 // elem(pos) = map[pos] (map == nullptr: identity), pos < n.
 int soa_gather(const double* src, int comps, const int* map, long long n, long long stride, double* dst,

@@ -202,6 +202,13 @@ struct symel_cuda_ctx {
   static constexpr int kAux = 3;
   cudaStream_t aux[kAux] = {};
   cudaEvent_t fork_ev = nullptr, join_ev[kAux] = {};
+  // asynchronous tail of a deterministic assemble: E and the gradient are final before the
+  // Hessian fix-up; assemble() returns then, the Hessian fix-up keeps running on `stream`
+  // (every later call that reads the matrix is ordered after it) and copy_gradient reads the
+  // gradient on copy_stream once grad_ready has fired
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t grad_ready = nullptr, e_ready = nullptr;
+  bool timings_pending = false;
   dev::SolverWork solver;      // SpMV / PCG work vectors
 };
 
@@ -729,7 +736,7 @@ int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
   return v;
 }
 
-double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st);
+double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st, bool async_tail = false);
 
 
 bool all_tile_capable(symel_cuda_ctx* c) {
@@ -899,10 +906,11 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
       CK(cudaStreamWaitEvent(c->stream, c->join_ev[i], 0));
     }
   cudaEventRecord(c->ev[1], c->stream);
+  // gradient rows first, then the energy: both final before the (larger) Hessian fix-up
+  const bool async_tail = !atomic && !c->any_pins && !std::getenv("SYMEL_SYNC_ASSEMBLE");
   if (!atomic) {
-    CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream));
-    c->launches += (c->tplan.h.n_pt > 0) + (c->tplan.g.n_pt > 0) + (c->tplan.h.n_untouched > 0) +
-                   (c->tplan.g.n_untouched > 0);
+    CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream, 2));
+    c->launches += (c->tplan.g.n_pt > 0) + (c->tplan.g.n_untouched > 0);
   }
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
@@ -914,10 +922,25 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
   }
   CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
   ++c->launches;
+  if (async_tail) {
+    const int nen = (int)c->energies.size();
+    CK(cudaEventRecord(c->grad_ready, c->stream));
+    CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + nen, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * nen, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(c->e_ready, c->stream));
+    CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream, 1));
+    c->launches += (c->tplan.h.n_pt > 0) + (c->tplan.h.n_untouched > 0);
+    return finish_assemble(c, st, true);
+  }
+  if (!atomic) {
+    CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream, 1));
+    c->launches += (c->tplan.h.n_pt > 0) + (c->tplan.h.n_untouched > 0);
+  }
   if (c->any_pins) {
     CK(dev::apply_pins(c->d_pins, c->n_rows, c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->d_grad, c->stream));
     ++c->launches;
   }
+  CK(cudaEventRecord(c->grad_ready, c->stream));
   return finish_assemble(c, st);
 }
 
@@ -1051,17 +1074,30 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
 }
 
 // E + finiteness readback, timings, the check_finite contract (assembly.hpp:426-438).
-double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st) {
-  const int ne = (int)c->energies.size();
-  cudaEventRecord(c->ev[2], c->stream);
-  CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * ne, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+void settle_timings(symel_cuda_ctx* c) {
+  if (!c->timings_pending) return;
+  cudaEventSynchronize(c->ev[2]);
   float m1 = 0, m2 = 0;
   cudaEventElapsedTime(&m1, c->ev[0], c->ev[1]);
   cudaEventElapsedTime(&m2, c->ev[1], c->ev[2]);
   c->timings.eval_ms = m1;
   c->timings.assemble_ms = m2;
+  c->timings_pending = false;
+}
+
+double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st, bool async_tail) {
+  const int ne = (int)c->energies.size();
+  if (async_tail) {  // E / bad already copied behind e_ready; the Hessian fix-up runs on
+    cudaEventRecord(c->ev[2], c->stream);
+    CK(cudaEventSynchronize(c->e_ready));
+  } else {
+    cudaEventRecord(c->ev[2], c->stream);
+    CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * ne, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  c->timings_pending = true;
+  if (!async_tail) settle_timings(c);
   const double E = c->h_pinned[0];
   const int* bad = reinterpret_cast<const int*>(c->h_pinned + 1);
   if (st) *st = symel_cuda_status{SYMEL_OK, -1, -1};
@@ -1168,6 +1204,9 @@ int symel_cuda_create(int device, symel_cuda_ctx** out) {
     for (auto& ev : c->ev) cudaEventCreate(&ev);
     for (auto& st : c->aux) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c->grad_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->e_ready, cudaEventDisableTiming);
     for (auto& ev : c->join_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   }
   if (const char* d = std::getenv("SYMEL_CUDA_CACHE")) c->cache_dir = d;
@@ -1198,6 +1237,9 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     for (auto& ev : c->ev) if (ev) cudaEventDestroy(ev);
     for (auto& ev : c->join_ev) if (ev) cudaEventDestroy(ev);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    if (c->grad_ready) cudaEventDestroy(c->grad_ready);
+    if (c->e_ready) cudaEventDestroy(c->e_ready);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto& st : c->aux) if (st) cudaStreamDestroy(st);
     cudaStreamDestroy(c->stream);
   }
@@ -1243,8 +1285,11 @@ int symel_cuda_set_array(symel_cuda_ctx* c, int id, const double* host, uint64_t
     Array& a = array_of(c, id);
     if (count != a.items * a.comps) throw Fail{SYMEL_E_ARG, "array '" + a.name + "': size mismatch"};
     if (c->device < 0) throw Fail{SYMEL_E_NODEVICE, "no CUDA device"};
-    CK(cudaMemcpyAsync(a.d, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    // on the copy stream, after the last assemble's element kernels (grad_ready): the upload
+    // overlaps a still running Hessian fix-up, which never reads the state arrays
+    CK(cudaStreamWaitEvent(c->copy_stream, c->grad_ready, 0));
+    CK(cudaMemcpyAsync(a.d, host, sizeof(double) * count, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaStreamSynchronize(c->copy_stream));
     ++a.version;
   });
 }
@@ -1490,8 +1535,10 @@ int symel_cuda_copy_pattern(symel_cuda_ctx* c, int64_t* row_ptr, int64_t* col_id
 
 int symel_cuda_copy_gradient(symel_cuda_ctx* c, double* host) {
   return guarded(c, [&] {
-    CK(cudaMemcpyAsync(host, c->d_grad, sizeof(double) * c->n_dofs, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    // final once grad_ready fired (possibly while the Hessian fix-up still runs)
+    CK(cudaStreamWaitEvent(c->copy_stream, c->grad_ready, 0));
+    CK(cudaMemcpyAsync(host, c->d_grad, sizeof(double) * c->n_dofs, cudaMemcpyDeviceToHost, c->copy_stream));
+    CK(cudaStreamSynchronize(c->copy_stream));
   });
 }
 
@@ -1675,7 +1722,10 @@ int symel_cuda_element_outputs(symel_cuda_ctx* c, int eid, uint64_t first, uint6
 }
 
 int symel_cuda_get_timings(symel_cuda_ctx* c, symel_cuda_timings* t) {
-  return guarded(c, [&] { *t = c->timings; });
+  return guarded(c, [&] {
+    settle_timings(c);  // waits for the asynchronous Hessian fix-up of the last assemble
+    *t = c->timings;
+  });
 }
 
 int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* buf, uint64_t len, uint64_t* needed) {

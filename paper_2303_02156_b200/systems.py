@@ -106,6 +106,7 @@ class DeviceSystem:
         A.set_array(self.rest, case.X)
         p = case.params
         self.energies: Dict[str, int] = {}
+        self.arrays: Dict[str, int] = {"x": self.x, "rest": self.rest}
         flags = ENERGY_SPD if spd else 0
         if case.kind in ("tet4", "contact"):
             own = case.conn if n_own is None else case.conn[:n_own]
@@ -155,7 +156,7 @@ class DeviceSystem:
             self.energies["inertia"] = A.add_energy("inertia", vc, tapes("inertia"), inertia_inputs(self.x, xp, v, m),
                                                     range(3))
             npairs = ex["pairs"].shape[0]
-            off = A.add_array("pair_offset", npairs, 12)
+            off = self.arrays["pair_offset"] = A.add_array("pair_offset", npairs, 12)
             A.set_array(off, ex["offsets"])
             pc = A.add_connectivity("pairs", 4)
             A.set_elements(pc, ex["pairs"])

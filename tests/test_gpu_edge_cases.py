@@ -1,0 +1,129 @@
+"""GPU edge cases through the generic C-ABI registration (DeviceAssembler), each against the C
+oracle built with the identical registration:
+
+* b = 1: the tet tape bound to a 1-component dof array (12 "nodes" per element), so the
+  assembly.hpp:273-276 rule picks scalar blocks -- pattern, gradient and values;
+* an energy with no elements next to a populated one; nodes no element touches (their diagonal
+  block exists and is zero, assembly.hpp:299-300);
+* contact pairs that are all inactive (activation empties the energy) and a second assemble
+  after re-activating them (pattern rebuilt).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_tape
+from paper_2303_02156_b200 import configs as C
+from paper_2303_02156_b200 import systems as S
+from paper_2303_02156_b200.device import DeviceAssembler, IN_ITEM
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+MODES = ["ordered", "deterministic", "atomic"]
+
+
+def check(dev, ref, oracle_mod, tol=TOL):
+    E, g, H = dev
+    assert H.b == ref["b"]
+    np.testing.assert_array_equal(H.row_ptr, ref["row_ptr"])
+    np.testing.assert_array_equal(H.col_idx, ref["col_idx"])
+    assert abs(E - ref["E"]) / max(1.0, abs(ref["E"])) <= tol
+    assert oracle_mod.rel_err(g, ref["grad"]) <= tol
+    assert oracle_mod.rel_err(H.values, ref["vals"]) <= tol
+
+
+def device_result(A, mode):
+    E = A.assemble(mode)
+    return E, A.gradient(), A.hessian()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_scalar_blocks_b1(mode, oracle_mod):
+    case = C.tet4_case(3, name="b1")
+    p = case.params
+    n = case.n_nodes
+    # every tet "node" dof becomes its own item of a 1-component array
+    conn12 = (case.conn[:, :, None] * 3 + np.arange(3)[None, None, :]).reshape(-1, 12)
+    x1 = case.x.reshape(-1, 1)
+    conn_both = np.concatenate([conn12, case.conn], axis=1)  # slots 0-11: scalar dofs, 12-15: rest nodes
+    inputs = [(IN_ITEM, 0, k, 0) for k in range(12)] + [(IN_ITEM, 1, 12 + a, c) for a in range(4) for c in range(3)] \
+        + [(S.IN_PARAM, 0, 0, 0)] * 2
+    A = DeviceAssembler()
+    xa = A.add_array("x", 3 * n, 1, True)
+    ra = A.add_array("rest", n, 3)
+    A.set_array(xa, x1)
+    A.set_array(ra, case.X)
+    cid = A.add_connectivity("tets", 16)
+    A.set_elements(cid, conn_both)
+    A.add_energy("elastic", cid, golden_tape("tet4_elastic"), inputs, range(12), params={24: p["mu"], 25: p["lambda"]})
+    from oracle import oracle as O
+    sysm = O.System()
+    ox = sysm.add_array("x", x1, 1, True)
+    orr = sysm.add_array("rest", case.X, 3)
+    sysm.add_energy("elastic", conn_both, 16, golden_tape("tet4_elastic"), inputs, range(12),
+                    params={24: p["mu"], 25: p["lambda"]})
+    ref = sysm.assemble()
+    assert ref["b"] == 1
+    check(device_result(A, mode), ref, oracle_mod, 1e-13 if mode == "ordered" else TOL)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_empty_energy_and_isolated_nodes(mode, oracle_mod):
+    case = C.tet4_case(3, name="iso")
+    p = case.params
+    extra = 7                                  # nodes no element touches
+    x = np.concatenate([case.x, np.random.default_rng(3).random((extra, 3))])
+    X = np.concatenate([case.X, np.random.default_rng(4).random((extra, 3))])
+    A = DeviceAssembler()
+    xa = A.add_array("x", x.shape[0], 3, True)
+    ra = A.add_array("rest", x.shape[0], 3)
+    A.set_array(xa, x)
+    A.set_array(ra, X)
+    t = A.add_connectivity("tets", 4)
+    A.set_elements(t, case.conn)
+    A.add_energy("elastic", t, golden_tape("tet4_elastic"), S.solid_tet_inputs(xa, ra), range(12),
+                 params={24: p["mu"], 25: p["lambda"]})
+    t0 = A.add_connectivity("none", 4)
+    A.set_elements(t0, np.zeros((0, 4), np.int64))
+    A.add_energy("empty", t0, golden_tape("tet4_elastic"), S.solid_tet_inputs(xa, ra), range(12),
+                 params={24: p["mu"], 25: p["lambda"]})
+    from oracle import oracle as O
+    sysm = O.System()
+    ox = sysm.add_array("x", x, 3, True)
+    orr = sysm.add_array("rest", X, 3)
+    sysm.add_energy("elastic", case.conn, 4, golden_tape("tet4_elastic"), S.solid_tet_inputs(ox, orr), range(12),
+                    params={24: p["mu"], 25: p["lambda"]})
+    sysm.add_energy("empty", np.zeros((0, 4), np.int64), 4, golden_tape("tet4_elastic"), S.solid_tet_inputs(ox, orr),
+                    range(12), params={24: p["mu"], 25: p["lambda"]})
+    ref = sysm.assemble()
+    E, g, H = device_result(A, mode)
+    check((E, g, H), ref, oracle_mod, 1e-13 if mode == "ordered" else TOL)
+    n = case.n_nodes
+    for r in range(n, n + extra):  # isolated rows: the diagonal block only, zero
+        k0, k1 = H.row_ptr[r], H.row_ptr[r + 1]
+        assert k1 - k0 == 1 and H.col_idx[k0] == r
+        assert not np.any(H.values.reshape(-1, 9)[k0])
+    assert not np.any(g[3 * n:])
+
+
+def test_all_pairs_inactive_then_active(oracle_mod):
+    case = C.config5(3, 30)
+    off = case.extra["offsets"].reshape(-1, 4, 3).copy()
+    q = case.x[case.extra["pairs"]] + off
+    nrm = np.cross(q[:, 2] - q[:, 1], q[:, 3] - q[:, 1])
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    far = off.copy()
+    far[:, 0] += 5e-3 * nrm                    # every point beyond d_hat: nothing active
+    inactive = C.Case(case.name, case.kind, case.x, case.X, case.conn, case.params,
+                      dict(case.extra, offsets=far.reshape(-1, 12)))
+    ds = S.DeviceSystem(inactive)
+    from oracle import oracle as O
+    for mode in MODES:
+        ref = O.system_for_case(inactive, golden_tape).assemble()
+        check(device_result(ds.asm, mode), ref, oracle_mod, 1e-13 if mode == "ordered" else TOL)
+        assert ds.asm.active_count(ds.energies["contact"]) == 0
+    # back in range: activation refresh rebuilds the pattern with the pairs
+    ds.asm.set_array(ds.arrays["pair_offset"], case.extra["offsets"])
+    ref = O.system_for_case(case, golden_tape).assemble()
+    for mode in MODES:
+        check(device_result(ds.asm, mode), ref, oracle_mod, 1e-13 if mode == "ordered" else TOL)
+    assert ds.asm.active_count(ds.energies["contact"]) == 30

@@ -127,3 +127,19 @@ def test_all_pairs_inactive_then_active(oracle_mod):
     for mode in MODES:
         check(device_result(ds.asm, mode), ref, oracle_mod, 1e-13 if mode == "ordered" else TOL)
     assert ds.asm.active_count(ds.energies["contact"]) == 30
+
+
+@pytest.mark.parametrize("mode", ["deterministic", "atomic"])
+def test_topology_change(mode, oracle_mod):
+    """New connectivity on a live context (the reference's topology stamp, assembly.hpp:207-225):
+    the pattern, slot maps and tile plan are rebuilt and results follow the new element set."""
+    case = C.tet4_case(4, name="topo")
+    p = case.params
+    ds = S.DeviceSystem(case)
+    ds.asm.assemble(mode)
+    from oracle import oracle as O
+    for keep in (case.conn[::2], case.conn[1::3], case.conn):
+        ds.asm.set_elements(0, keep)  # connectivity 0 = "tets"
+        sub = C.Case(case.name, case.kind, case.x, case.X, keep, p)
+        ref = O.system_for_case(sub, golden_tape).assemble()
+        check(device_result(ds.asm, mode), ref, oracle_mod)

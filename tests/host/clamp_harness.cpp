@@ -8,6 +8,13 @@
 #define __device__
 #define __forceinline__ inline
 static inline double sy_rcp(double x) { return 1.0 / x; }
+// the device QL keeps a warp at level L while any lane still iterates there (lookahead lanes
+// work on L+1 meanwhile); a single host lane emulates that with randomly busy warp-mates
+static unsigned sy_host_rng = 12345u;
+static inline bool sy_host_any(bool mine) {
+  sy_host_rng = sy_host_rng * 1103515245u + 12345u;
+  return mine || ((sy_host_rng >> 16) % 3u) == 0u;
+}
 #include "clamp_fragment.inc"
 
 template <int N>

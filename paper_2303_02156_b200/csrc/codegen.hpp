@@ -50,6 +50,7 @@ struct KernelSpec {
   OutMode mode = OutMode::contrib;
   bool fast = true;        // division strength reduction + FMA contraction
   std::uint32_t spd_m = 0; // fused_tile_spd: size m of the reduced eigenproblem
+  bool spd_lookahead = true;  // fused_tile_spd: QL with per-lane level lookahead (sy_ql_la)
   bool stage_global = false;  // tile modes: stage element outputs in global memory (large elements)
   int item_lanes = 1;         // tile mode with fixed summation: the n_items terms of an element
                               // run on adjacent lanes (one term each) and are summed in order

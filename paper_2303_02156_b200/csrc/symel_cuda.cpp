@@ -470,6 +470,10 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.soa_arrays = soa_arrays_of(c, e);
       s.mode = OutMode::fused_tile_spd;
       s.spd_m = e.spd_info.frontier;
+      // QL lookahead (codegen.cpp sy_ql_la) pays off where divergence in the QL dominates
+      // (config 2 tets: 8.66 -> 7.20 ms); the exact-rounding contact kernel, whose larger
+      // unfactorised tape already strains the instruction cache, measured 1.4 ms slower with it
+      s.spd_lookahead = !(e.flags & SYMEL_ENERGY_EXACT) && !std::getenv("SYMEL_NO_QL_LOOKAHEAD");
       s.schedule = -1;
       s.threads_per_block = kTileElems;
       s.min_blocks = 2;

@@ -1,9 +1,9 @@
 """Source-region breakdown of an ncu --set full capture of a generated tile kernel: warp-stall
 samples, executed warp instructions and SIMT efficiency per region of the generated source
 (eigen fragment, element tape, SPD tail, tile reduction). usage: ncu_regions.py REP SRC.cu"""
-import csv, subprocess, sys
+import csv, os, subprocess, sys
 rep, srcf = sys.argv[1], sys.argv[2]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
+out = subprocess.run(["ncu", "-i", rep] + os.environ.get("NCU_FILTER", "").split() + [ "--page", "source", "--csv", "--print-source", "cuda,sass",
                       "--resolve-source-file", srcf], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 hdr = next(r for r in rows if r and r[0] == "Line No")

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <fstream>
 #include <iostream>
+#include <string>
 #define __device__
 #define __forceinline__ inline
 static inline double sy_rcp(double x) { return 1.0 / x; }
@@ -17,7 +18,7 @@ static inline bool sy_host_any(bool mine) {
 }
 #include "clamp_fragment.inc"
 
-template <int N>
+template <int N, bool LA>
 static int run() {
   double A[N][N];
   int count = 0;
@@ -28,7 +29,7 @@ static int run() {
     double d[N], e[N];
     double V[N][N];
     for (int i = 0; i < N; ++i) for (int j = 0; j < N; ++j) V[i][j] = A[i][j];
-    sy_eig<N>(V, d, e);
+    sy_eig<N, LA>(V, d, e);
     // clamp(M) = V max(d, 0) V^T, as the fused tile kernel rebuilds it (codegen emit_spd_tail)
     for (int i = 0; i < N; ++i)
       for (int j = 0; j <= i; ++j) {
@@ -43,13 +44,15 @@ static int run() {
 }
 
 int main(int argc, char** argv) {
+  // argv[2] = "la": the lookahead QL variant (sy_ql_la), else the plain one (sy_ql)
   const int n = std::atoi(argv[1]);
+  const bool la = argc > 2 && std::string(argv[2]) == "la";
   switch (n) {
-    case 2: run<2>(); break;
-    case 3: run<3>(); break;
-    case 4: run<4>(); break;
-    case 6: run<6>(); break;
-    case 9: run<9>(); break;
+    case 2: la ? run<2, true>() : run<2, false>(); break;
+    case 3: la ? run<3, true>() : run<3, false>(); break;
+    case 4: la ? run<4, true>() : run<4, false>(); break;
+    case 6: la ? run<6, true>() : run<6, false>(); break;
+    case 9: la ? run<9, true>() : run<9, false>(); break;
     default: return 2;
   }
   return 0;

@@ -34,10 +34,10 @@ def harness(tmp_path_factory):
     return str(exe)
 
 
-def run(exe, mats):
+def run(exe, mats, variant=""):
     n = mats.shape[1]
     txt = "\n".join(" ".join("%.17g" % v for v in m.ravel()) for m in mats)
-    out = subprocess.run([exe, str(n)], input=txt, capture_output=True,
+    out = subprocess.run([exe, str(n)] + ([variant] if variant else []), input=txt, capture_output=True,
                          text=True, check=True).stdout
     return np.array(out.split(), dtype=np.float64).reshape(mats.shape)
 
@@ -86,11 +86,14 @@ def cases(rng, n):
     return np.array(out)
 
 
+@pytest.mark.parametrize("variant", ["plain", "la"])
 @pytest.mark.parametrize("n", [2, 3, 4, 6, 9])
-def test_clamp_matches_eigh(harness, n):
+def test_clamp_matches_eigh(harness, n, variant):
+    """Both QL variants: sy_ql and the lookahead sy_ql_la (its warp-mates emulated by a random
+    vote in the host harness, so lookahead sweeps are exercised)."""
     rng = np.random.default_rng(1234 + n)
     mats = cases(rng, n)
-    got = run(harness, mats)
+    got = run(harness, mats, variant)
     worst = 0.0
     for m, g in zip(mats, got):
         ref = clamp_ref(m)
@@ -98,3 +101,12 @@ def test_clamp_matches_eigh(harness, n):
         worst = max(worst, np.abs(g - ref).max() / scale)
         assert np.allclose(g, g.T, rtol=0, atol=1e-14 * scale)
     assert worst <= 1e-10, worst
+
+
+@pytest.mark.parametrize("n", [3, 9])
+def test_lookahead_is_bitwise_the_plain_ql(harness, n):
+    """The lookahead only reschedules sweeps across a warp: every lane runs the same arithmetic
+    in the same order as sy_ql, so the results are bit-identical."""
+    rng = np.random.default_rng(99 + n)
+    mats = cases(rng, n)
+    assert np.array_equal(run(harness, mats, "plain"), run(harness, mats, "la"))

@@ -19,9 +19,11 @@ for r in rows:
 src = open(srcf).read().splitlines()
 marks = {"prelude (rcp/rsqrt helpers)": 1}
 for i, l in enumerate(src, 1):
-    if "void sy_eig(" in l: marks["eigen: Householder tridiagonalisation"] = i
+    if "void sy_tred2(" in l: marks["eigen: Householder tridiagonalisation"] = i
+    if "void sy_ql(" in l: marks["eigen: implicit QL with vectors"] = i
+    if "void sy_ql_la(" in l: marks["eigen: implicit QL with vectors (lookahead)"] = i
+    if "void sy_eig(" in l: marks["eigen: wrapper"] = i
     if "V[N - 1][i] = V[i][i]" in l: marks["eigen: accumulate Q"] = i
-    if "double f = 0.0, tst1 = 0.0;" in l: marks["eigen: implicit QL with vectors"] = i
     if "const long long e =" in l: marks["element tape (E, g, M, W)"] = i
     if "sy_eig<" in l and "call" not in l: marks["SPD tail: clamp + H = W^T C W + stage"] = i - 1
     if "cp.async.wait_all" in l: marks["tile reduction + energy"] = i

@@ -300,8 +300,9 @@ def main():
             "achieved_without_spd": achieved_nospd, "frac_without_spd": achieved_nospd / peak}
     facts_path = os.path.join(ROOT, "profiles", "kernel_facts.json")
     if os.path.exists(facts_path):
-        facts = json.load(open(facts_path)).get(args.config)
-        if facts and (spd or args.config != "c2"):
+        key = args.config if (spd or args.config != "c2") else "c2_nospd"
+        facts = json.load(open(facts_path)).get(key)
+        if facts:
             roof["traffic"] = facts["traffic_bytes"]
             roof["ncu"] = {k: v for k, v in facts.items() if k != "traffic_bytes"}
 

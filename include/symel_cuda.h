@@ -181,7 +181,10 @@ int symel_cuda_copy_active(symel_cuda_ctx* ctx, int energy_id, uint8_t* mask);
 int symel_cuda_element_outputs(symel_cuda_ctx* ctx, int energy_id, uint64_t first, uint64_t count,
                                uint32_t flags, double* out);
 int symel_cuda_get_timings(symel_cuda_ctx* ctx, symel_cuda_timings* t);
-/* Generated CUDA source of an energy's derivative kernel for a mode (debug / tests). */
+/* Generated CUDA source of an energy's derivative kernel for a mode (debug / tests / profiling).
+ * flags: the assembly mode, | SYMEL_SRC_PLAN_GLOBAL for the tile kernel variant that reads
+ * its plan slice from L2 (the one assemble picks when the slice does not fit shared memory). */
+#define SYMEL_SRC_PLAN_GLOBAL 0x100u
 int symel_cuda_kernel_source(symel_cuda_ctx* ctx, int energy_id, uint32_t flags, char* buf,
                              uint64_t buf_len, uint64_t* needed);
 typedef struct {

@@ -1740,9 +1740,10 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
     // shared memory)
     const std::uint32_t mode = flags & 3u;
     Variant v = mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : (mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : V_CONTRIB_FAST);
+    const bool g = flags & SYMEL_SRC_PLAN_GLOBAL;
     if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
-      if (!(e.flags & SYMEL_ENERGY_SPD)) v = V_TILE;
-      else if (spd_tape(e)) v = V_TILE_SPD;
+      if (!(e.flags & SYMEL_ENERGY_SPD)) v = g ? V_TILE_G : V_TILE;
+      else if (spd_tape(e)) v = g ? V_TILE_SPD_G : V_TILE_SPD;
     }
     const KernelSpec s = spec_for(c, e, v);
     const std::string src = emit_kernel(s);

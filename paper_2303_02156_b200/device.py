@@ -416,9 +416,11 @@ class DeviceAssembler:
     def sync(self) -> None:
         self._check(self.lib.symel_cuda_sync(self.h))
 
-    def kernel_source(self, eid: int, mode: str = "deterministic") -> str:
+    def kernel_source(self, eid: int, mode: str = "deterministic", plan_global: bool = False) -> str:
+        """Generated source; plan_global: the tile variant reading its plan slice from L2."""
+        fl = MODES[mode] | (0x100 if plan_global else 0)  # SYMEL_SRC_PLAN_GLOBAL
         need = C.c_uint64()
-        self._check(self.lib.symel_cuda_kernel_source(self.h, eid, MODES[mode], None, 0, C.byref(need)))
+        self._check(self.lib.symel_cuda_kernel_source(self.h, eid, fl, None, 0, C.byref(need)))
         buf = C.create_string_buffer(need.value)
-        self._check(self.lib.symel_cuda_kernel_source(self.h, eid, MODES[mode], buf, need.value, None))
+        self._check(self.lib.symel_cuda_kernel_source(self.h, eid, fl, buf, need.value, None))
         return buf.value.decode()

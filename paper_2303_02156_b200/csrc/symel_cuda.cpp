@@ -242,6 +242,8 @@ Energy& energy_of(symel_cuda_ctx* c, int id) {
 
 // ------------------------------------------------------------------------------ NVRTC
 
+constexpr int kNoBadElem = 0x7f7f7f7f;  // d_bad sentinel (memset 0x7f)
+
 Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
   std::string src = emit_kernel(spec);
   const std::string flags = "fmad1";
@@ -963,8 +965,9 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
     CK(cudaMallocHost((void**)&c->h_pinned, 1024));
   }
   if (ne > 60) throw Fail{SYMEL_E_ARG, "too many energies"};
-  std::vector<int> init(ne, INT_MAX);
-  CK(cudaMemcpyAsync(c->d_bad, init.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, c->stream));
+  // "no non-finite element" sentinel (every byte 0x7f: larger than any element id), set without
+  // a host->device copy
+  CK(cudaMemsetAsync(c->d_bad, 0x7f, sizeof(int) * ne, c->stream));
   CK(cudaMemsetAsync(c->d_energy, 0, sizeof(double) * (ne + 1), c->stream));
   // fast modes run the tile kernel (K3) when every energy's staged element fits a CTA
   bool any_spd = false;
@@ -1106,7 +1109,7 @@ double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st, bool async_tail
   const int* bad = reinterpret_cast<const int*>(c->h_pinned + 1);
   if (st) *st = symel_cuda_status{SYMEL_OK, -1, -1};
   for (int q = 0; q < ne; ++q) {
-    if (bad[q] != INT_MAX) {
+    if (bad[q] != kNoBadElem) {
       const Energy& e = *c->energies[q];
       const int64_t el = element_of(c, e, bad[q]);
       if (st) *st = symel_cuda_status{SYMEL_E_NONFINITE, q, el};

@@ -32,7 +32,12 @@ sys.path.insert(0, ROOT)
 FLOPS = {"tet4": 4406 + 157, "tet10": 4 * 23164 + 3 * 931 + 931, "membrane": 5622 + 91, "bending": 1009 + 157,
          "contact": 2811 + 157, "inertia": 23 + 13}
 # compulsory bytes per element: unique inputs once + unique outputs once
-BYTES = {"c1": 223.0, "c2": 211.0, "c3": 2941.0, "c4": 163.0, "c5": 211.0}
+# (tets and tet10: connectivity, x, X, their share of the BSR values and the gradient)
+BYTES = {"tet4_c1": 223.0, "tet4": 211.0, "tet10": 2941.0,
+         "membrane": 12 + 40,      # connectivity + Dm2inv / area (x, BSR, g counted once below)
+         "bending": 16 + 1152,     # connectivity + the 144-double Q of the flap
+         "contact": 16 + 96 + 16 * 72,  # connectivity + per-pair offsets + its 16 scattered blocks
+         "inertia": 56 + 72}       # x_prev, v, m + the diagonal block
 
 
 def parse():
@@ -89,6 +94,29 @@ def flops_per_step(cfg: str, case) -> float:
         return FLOPS["membrane"] * case.conn.shape[0] + FLOPS["bending"] * case.extra["flaps"].shape[0]
     return (FLOPS["tet4"] * case.conn.shape[0] + FLOPS["contact"] * case.extra["pairs"].shape[0]
             + FLOPS["inertia"] * case.n_nodes)
+
+
+def hbm_peak_gbs() -> float:
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written); else the profiling
+    recipe's fallback (6.65 TB/s)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def bytes_per_step(cfg: str, case) -> float:
+    """Compulsory HBM bytes of one assemble: unique inputs read once + unique
+    outputs written once; the static pattern and the tile plan (as-implemented extras) excluded."""
+    if case.kind == "tet4":
+        return BYTES["tet4_c1" if cfg == "c1" else "tet4"] * case.conn.shape[0]
+    if case.kind == "tet10":
+        return BYTES["tet10"] * case.conn.shape[0]
+    if case.kind == "cloth":
+        shared = 72.0 * 10_984_004 * case.n_nodes / 1_000_000 + 2 * 24.0 * case.n_nodes  # BSR + g + x
+        return (BYTES["membrane"] * case.conn.shape[0] + BYTES["bending"] * case.extra["flaps"].shape[0] + shared)
+    return (BYTES["tet4"] * case.conn.shape[0] + BYTES["contact"] * case.extra["pairs"].shape[0]
+            + BYTES["inertia"] * case.n_nodes)
 
 
 class ClockSampler:
@@ -298,6 +326,17 @@ def main():
                                 + (f" + P_spd = 10*{SPD_N}^3 = {P_SPD} per projected element (standard symmetric "
                                    "eigen-decomposition with vectors + rebuild)" if spd else ""),
             "achieved_without_spd": achieved_nospd, "frac_without_spd": achieved_nospd / peak}
+    # the element roofline is the slower of its flops at the FP64 peak and its compulsory bytes at
+    # the HBM bandwidth (north star); config 4 (the 1152-byte bending Q per flap) is HBM-bound
+    by = bytes_per_step(args.config, case)
+    bw = hbm_peak_gbs()
+    roof["algorithmic_bytes_per_step"] = by
+    roof["hbm_achieved_gbs"] = by / (k_ms * 1e-3) / 1e9
+    roof["hbm_frac"] = roof["hbm_achieved_gbs"] / bw
+    if by / (bw * 1e9) > (fl + fl_spd) / (peak * 1e12):
+        roof.update({"bound": "hbm", "achieved": roof["hbm_achieved_gbs"], "peak": bw, "unit": "GB/s",
+                     "frac": roof["hbm_frac"], "fp64_frac": achieved / peak,
+                     "peak_source": "HBM copy bandwidth of measured (MEASURED_PEAKS.json hbm_gbs)"})
     facts_path = os.path.join(ROOT, "profiles", "kernel_facts.json")
     if os.path.exists(facts_path):
         key = args.config if (spd or args.config != "c2") else "c2_nospd"

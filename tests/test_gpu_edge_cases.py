@@ -143,3 +143,44 @@ def test_topology_change(mode, oracle_mod):
         sub = C.Case(case.name, case.kind, case.x, case.X, keep, p)
         ref = O.system_for_case(sub, golden_tape).assemble()
         check(device_result(ds.asm, mode), ref, oracle_mod)
+
+
+def _assemble_with_env(case, spd, env, mode="deterministic"):
+    """A fresh context built while `env` is set (the code generator reads its diagnostic
+    switches when it specialises a kernel)."""
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        ds = S.DeviceSystem(case, tapes=S.default_tapes(), spd=spd)
+        E = ds.asm.assemble(mode)
+        return E, ds.asm.gradient(), ds.asm.hessian()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_ql_lookahead_is_bitwise_the_plain_ql():
+    """The per-lane QL lookahead (codegen sy_ql_la) only reschedules sweeps across a warp; on the
+    device too the projected Hessian is bit-identical to the plain QL's (sy_ql)."""
+    case = C.config2(6)
+    E0, g0, H0 = _assemble_with_env(case, True, {})
+    E1, g1, H1 = _assemble_with_env(case, True, {"SYMEL_NO_QL_LOOKAHEAD": "1"})
+    assert E0 == E1
+    np.testing.assert_array_equal(g0, g1)
+    np.testing.assert_array_equal(H0.values, H1.values)
+
+
+def test_item_lane_reduce_scatter_matches_sequential_item_sum(oracle_mod):
+    """tet10's quadrature terms summed by the four-lane reduce-scatter (pairwise order) against
+    the per-output shuffle tree (the reference's sequential order): equal to rounding."""
+    case = C.config3(3)
+    E0, g0, H0 = _assemble_with_env(case, False, {})
+    E1, g1, H1 = _assemble_with_env(case, False, {"SYMEL_NO_QUAD_REDUCE": "1"})
+    np.testing.assert_array_equal(H0.col_idx, H1.col_idx)
+    assert abs(E0 - E1) <= 1e-13 * max(1.0, abs(E1))
+    assert oracle_mod.rel_err(g0, g1) <= 1e-13
+    assert oracle_mod.rel_err(H0.values, H1.values) <= 1e-13

@@ -181,6 +181,9 @@ struct symel_cuda_ctx {
   bool refs_valid = false;
   dev::TilePlan tplan;
   bool tplan_valid = false;
+  cudaGraphExec_t graph_exec = nullptr;  // recorded tiled assemble (assemble_tiled)
+  std::string graph_sig;                 // its launch signature (tiled_signature)
+  long long graph_launches = 0;          // kernels it launches
   std::uint64_t plan_epoch = 0;  // bumped on every tile-plan build (tile order may change)
   double* d_partials = nullptr;
   double* d_gpartials = nullptr;
@@ -837,35 +840,39 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
 
 // Fast path: one tile kernel per energy (eval + in-CTA reduction), then the fixed-order
 // fix-up of shared blocks (deterministic) or nothing (atomic: per-tile red.add).
-double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
+//
+// The launch sequence of an assemble is a pure function of the context state (buffers, plan,
+// kernel arguments incl. the params read at every assemble). It is recorded once as a CUDA
+// graph and replayed while that state is unchanged -- one host launch per assemble instead of
+// ~12 API calls (small meshes are host-bound: config 1's kernels take 30 of its ~90 us).
+
+struct TileLaunch {
+  Compiled* k = nullptr;
+  SyArgs a;
+  std::size_t smem = 0;
+  int stream_slot = 0;  // 0 = main stream, i > 0 = aux[(i - 1) % kAux]
+};
+
+// Builds the per-energy tile launches (host only; SoA refresh and buffer allocation happen here,
+// before any capture).
+std::vector<TileLaunch> tile_launches(symel_cuda_ctx* c, bool atomic) {
+  std::vector<TileLaunch> out;
   const int ne = (int)c->energies.size();
-  cudaEventRecord(c->ev[0], c->stream);
-  if (atomic) {
-    CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
-    CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
-  }
-  // energy kernels on separate streams (round robin over main + aux)
   const bool concurrent = !std::getenv("SYMEL_SERIAL_ENERGIES");
-  bool aux_used[symel_cuda_ctx::kAux] = {};
   int slot = 0;
-  if (concurrent) CK(cudaEventRecord(c->fork_ev, c->stream));
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    cudaStream_t est = c->stream;
-    if (concurrent && slot > 0) {
-      const int i = (slot - 1) % symel_cuda_ctx::kAux;
-      est = c->aux[i];
-      if (!aux_used[i]) CK(cudaStreamWaitEvent(est, c->fork_ev, 0));
-      aux_used[i] = true;
-    }
+    TileLaunch L;
+    L.stream_slot = concurrent ? slot : 0;
     ++slot;
     const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
     Compiled* k = kernel_for(c, e, spd ? V_TILE_SPD : V_TILE);
-    SyArgs a;
+    SyArgs& a = L.a;
     fill_args(c, e, a);
     a.active = e.d_tile_perm ? e.d_tile_elems : e.d_active;  // elements in tile order
     ensure_soa(c, e);
+    ensure_elem_buffers(c, e, false);
     for (const auto& kv : e.d_soa) a.arr[kv.first] = kv.second;
     a.soa_n = e.soa_n;
     a.n = e.n_active;
@@ -904,16 +911,86 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     }
     if (k->smem + plan_bytes > kTileSmemOne)
       throw Fail{SYMEL_E_STATE, "energy '" + e.name + "': tile plan slice exceeds shared memory"};
-    launch(c, k, a, e.n_active, k->smem + plan_bytes, est);
+    L.k = k;
+    L.smem = k->smem + plan_bytes;
+    if (L.smem > 48 * 1024 && L.smem != k->smem_attr) {  // set here, outside any capture
+      CK(cudaKernelSetAttributeForDevice(k->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem,
+                                         c->device));
+      k->smem_attr = L.smem;
+    }
+    out.push_back(L);
+  }
+  return out;
+}
+
+// Everything the enqueued operations read from the host side: kernel handles and arguments
+// (params by value, device pointers, counts), the tile plan (pointers and counts), the
+// context's device buffers and the flags that change the sequence.
+std::string tiled_signature(const symel_cuda_ctx* c, const std::vector<TileLaunch>& ls, bool atomic,
+                            bool async_tail) {
+  std::string sig;
+  auto put = [&](const void* p, std::size_t n) { sig.append(static_cast<const char*>(p), n); };
+  const int flags[4] = {atomic, async_tail, c->any_pins, (int)c->energies.size()};
+  put(flags, sizeof flags);
+  for (const TileLaunch& L : ls) {
+    put(&L.k, sizeof L.k);
+    put(&L.a, sizeof L.a);
+    put(&L.smem, sizeof L.smem);
+    put(&L.stream_slot, sizeof L.stream_slot);
+  }
+  put(&c->tplan, sizeof c->tplan);
+  const void* bufs[] = {c->d_partials, c->d_gpartials, c->d_vals, c->d_grad, c->d_tileE, c->d_partial,
+                        c->d_energy, c->d_bad, c->h_pinned, c->d_pins, c->d_row_ptr, c->d_col_idx};
+  put(bufs, sizeof bufs);
+  const long long dims[4] = {c->b, c->n_blocks, c->n_dofs, c->n_rows};
+  put(dims, sizeof dims);
+  for (const auto& ep : c->energies) {
+    const long long v[3] = {ep->skip ? 1 : 0, ep->n_active, ep->tile_base};
+    put(v, sizeof v);
+  }
+  return sig;
+}
+
+// Events the host or other streams wait on: recorded as real event nodes when captured into
+// the assemble graph (a plain record inside a capture only orders the captured work).
+cudaError_t record_ext(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, s);
+}
+
+// The stream-ordered work of one tiled assemble (everything up to finish_assemble).
+void enqueue_tiled(symel_cuda_ctx* c, const std::vector<TileLaunch>& ls, bool atomic, bool async_tail) {
+  const int ne = (int)c->energies.size();
+  record_ext(c->ev[0], c->stream);
+  if (atomic) {
+    CK(cudaMemsetAsync(c->d_vals, 0, sizeof(double) * c->n_blocks * c->b * c->b, c->stream));
+    CK(cudaMemsetAsync(c->d_grad, 0, sizeof(double) * c->n_dofs, c->stream));
+  }
+  // energy kernels on separate streams (round robin over main + aux)
+  bool aux_used[symel_cuda_ctx::kAux] = {};
+  bool forked = false;
+  for (const TileLaunch& L : ls) {
+    cudaStream_t est = c->stream;
+    if (L.stream_slot > 0) {
+      if (!forked) CK(cudaEventRecord(c->fork_ev, c->stream));
+      forked = true;
+      const int i = (L.stream_slot - 1) % symel_cuda_ctx::kAux;
+      est = c->aux[i];
+      if (!aux_used[i]) CK(cudaStreamWaitEvent(est, c->fork_ev, 0));
+      aux_used[i] = true;
+    }
+    SyArgs a = L.a;
+    launch(c, L.k, a, a.n, L.smem, est);
   }
   for (int i = 0; i < symel_cuda_ctx::kAux; ++i)
     if (aux_used[i]) {
       CK(cudaEventRecord(c->join_ev[i], c->aux[i]));
       CK(cudaStreamWaitEvent(c->stream, c->join_ev[i], 0));
     }
-  cudaEventRecord(c->ev[1], c->stream);
+  record_ext(c->ev[1], c->stream);
   // gradient rows first, then the energy: both final before the (larger) Hessian fix-up
-  const bool async_tail = !atomic && !c->any_pins && !std::getenv("SYMEL_SYNC_ASSEMBLE");
   if (!atomic) {
     CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream, 2));
     c->launches += (c->tplan.g.n_pt > 0) + (c->tplan.g.n_untouched > 0);
@@ -922,21 +999,19 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
     const long long nt = (e.n_active + tile_elems(e) - 1) / tile_elems(e);
-    ensure_elem_buffers(c, e, false);
     CK(dev::tile_energy(c->d_tileE, e.tile_base, nt, c->d_partial, c->d_energy + q, c->stream));
     c->launches += 2;
   }
   CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
   ++c->launches;
   if (async_tail) {
-    const int nen = (int)c->energies.size();
-    CK(cudaEventRecord(c->grad_ready, c->stream));
-    CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + nen, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * nen, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaEventRecord(c->e_ready, c->stream));
+    CK(record_ext(c->grad_ready, c->stream));
+    CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_pinned + 1, c->d_bad, sizeof(int) * ne, cudaMemcpyDeviceToHost, c->stream));
+    CK(record_ext(c->e_ready, c->stream));
     CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream, 1));
     c->launches += (c->tplan.h.n_pt > 0) + (c->tplan.h.n_untouched > 0);
-    return finish_assemble(c, st, true);
+    return;
   }
   if (!atomic) {
     CK(dev::tile_fixup(c->tplan, c->d_partials, c->d_gpartials, c->b, c->d_vals, c->d_grad, c->stream, 1));
@@ -946,8 +1021,47 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     CK(dev::apply_pins(c->d_pins, c->n_rows, c->b, c->d_row_ptr, c->d_col_idx, c->d_vals, c->d_grad, c->stream));
     ++c->launches;
   }
-  CK(cudaEventRecord(c->grad_ready, c->stream));
-  return finish_assemble(c, st);
+  CK(record_ext(c->grad_ready, c->stream));
+}
+
+double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
+  const bool async_tail = !atomic && !c->any_pins && !std::getenv("SYMEL_SYNC_ASSEMBLE");
+  const std::vector<TileLaunch> ls = tile_launches(c, atomic);
+  const bool graphs = !std::getenv("SYMEL_NO_GRAPH");
+  if (!graphs) {
+    enqueue_tiled(c, ls, atomic, async_tail);
+    return finish_assemble(c, st, async_tail);
+  }
+  std::string sig = tiled_signature(c, ls, atomic, async_tail);
+  if (!c->graph_exec || sig != c->graph_sig) {
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+    c->graph_sig.clear();
+    const long long l0 = c->launches;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue_tiled(c, ls, atomic, async_tail);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamEndCapture(c->stream, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      c->graph_exec = nullptr;
+      throw Fail{SYMEL_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie)};
+    }
+    c->graph_sig = std::move(sig);
+    c->graph_launches = c->launches - l0;
+    c->launches = l0;
+  }
+  CK(cudaGraphLaunch(c->graph_exec, c->stream));
+  c->launches += c->graph_launches;
+  return finish_assemble(c, st, async_tail);
 }
 
 double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st) {
@@ -1233,6 +1347,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
       for (auto& kv : e->d_soa) cfree(kv.second);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
     if (c->refs_valid) dev::free_ordered_refs(&c->refs);
     if (c->tplan_valid) dev::free_tile_plan(&c->tplan);

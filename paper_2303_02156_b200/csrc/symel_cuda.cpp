@@ -181,9 +181,14 @@ struct symel_cuda_ctx {
   bool refs_valid = false;
   dev::TilePlan tplan;
   bool tplan_valid = false;
-  cudaGraphExec_t graph_exec = nullptr;  // recorded tiled assemble (assemble_tiled)
-  std::string graph_sig;                 // its launch signature (tiled_signature)
-  long long graph_launches = 0;          // kernels it launches
+  struct AsmGraph {
+    std::string sig;                 // launch signature (tiled_signature)
+    cudaGraphExec_t exec = nullptr;  // recorded tiled assemble (assemble_tiled)
+    long long launches = 0;          // kernels it launches
+    unsigned long long used = 0;     // last use (LRU)
+  };
+  std::vector<AsmGraph> graphs;      // a few recorded assembles (e.g. one per mode)
+  unsigned long long graph_clock = 0;
   std::uint64_t plan_epoch = 0;  // bumped on every tile-plan build (tile order may change)
   double* d_partials = nullptr;
   double* d_gpartials = nullptr;
@@ -1033,10 +1038,19 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     return finish_assemble(c, st, async_tail);
   }
   std::string sig = tiled_signature(c, ls, atomic, async_tail);
-  if (!c->graph_exec || sig != c->graph_sig) {
-    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-    c->graph_exec = nullptr;
-    c->graph_sig.clear();
+  symel_cuda_ctx::AsmGraph* gr = nullptr;
+  for (auto& g : c->graphs)
+    if (g.sig == sig) gr = &g;
+  if (!gr) {
+    // record: at most kGraphs kept (alternating modes replay without re-recording); the least
+    // recently used one is replaced
+    constexpr std::size_t kGraphs = 4;
+    if (c->graphs.size() >= kGraphs) {
+      auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                  [](const auto& x, const auto& y) { return x.used < y.used; });
+      if (lru->exec) cudaGraphExecDestroy(lru->exec);
+      c->graphs.erase(lru);
+    }
     const long long l0 = c->launches;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
     try {
@@ -1049,18 +1063,19 @@ double assemble_tiled(symel_cuda_ctx* c, bool atomic, symel_cuda_status* st) {
     }
     cudaGraph_t g = nullptr;
     CK(cudaStreamEndCapture(c->stream, &g));
-    const cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    symel_cuda_ctx::AsmGraph ng;
+    const cudaError_t ie = cudaGraphInstantiate(&ng.exec, g, 0);
     cudaGraphDestroy(g);
-    if (ie != cudaSuccess) {
-      c->graph_exec = nullptr;
-      throw Fail{SYMEL_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie)};
-    }
-    c->graph_sig = std::move(sig);
-    c->graph_launches = c->launches - l0;
+    if (ie != cudaSuccess) throw Fail{SYMEL_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie)};
+    ng.sig = std::move(sig);
+    ng.launches = c->launches - l0;
     c->launches = l0;
+    c->graphs.push_back(std::move(ng));
+    gr = &c->graphs.back();
   }
-  CK(cudaGraphLaunch(c->graph_exec, c->stream));
-  c->launches += c->graph_launches;
+  gr->used = ++c->graph_clock;
+  CK(cudaGraphLaunch(gr->exec, c->stream));
+  c->launches += gr->launches;
   return finish_assemble(c, st, async_tail);
 }
 
@@ -1347,7 +1362,9 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
       for (auto& kv : e->d_soa) cfree(kv.second);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
-    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     cfree(c->d_partial); cfree(c->d_energy); cfree(c->d_bad);
     if (c->refs_valid) dev::free_ordered_refs(&c->refs);
     if (c->tplan_valid) dev::free_tile_plan(&c->tplan);

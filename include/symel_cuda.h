@@ -81,9 +81,14 @@ int symel_cuda_abi_version(void);
 int symel_cuda_create(int device, symel_cuda_ctx** out);
 void symel_cuda_destroy(symel_cuda_ctx* ctx);
 const char* symel_cuda_last_error(const symel_cuda_ctx* ctx);
-/* Kernel cache directory for <digest>.<spec>.sm100a.cubin (cache.hpp:103-111 analogue);
+/* Kernel cache directory for <kernel_key>.<variant>.sm100a.cubin (cache.hpp:103-111 analogue);
    NULL or "" disables the disk cache. Default: $SYMEL_CUDA_CACHE or none. */
 int symel_cuda_set_cache_dir(symel_cuda_ctx* ctx, const char* dir);
+/* CacheStats (cache.hpp:17-24) of this context's kernel cache: {builds, memory_hits, disk_hits,
+   corrupt}. Entries are <kernel_key hex>.<variant>.sm100a.cubin + .meta, kernel_key = the tape's
+   digest (registry.hpp:415-428, stamped by KernelCache::get_or_build, cache.hpp:78); a corrupt
+   entry (meta mismatch, not an image, rejected by the driver) is a warning + rebuild. */
+int symel_cuda_cache_stats(symel_cuda_ctx* ctx, uint64_t* out4);
 
 /* ---- state arrays: EnergySystem::add_array / add_dof_array (registry.hpp:124-133) ----- */
 /* Dof arrays form the dof layout in registration order (registry.hpp:354-372). */

@@ -26,6 +26,7 @@ from oracle import oracle as O  # noqa: E402
 from paper_2303_02156_b200 import configs as C  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+TAPE_DIR = os.path.join(ROOT, "paper_2303_02156_b200", "tapes")  # the reference's own tapes, shipped with the package
 
 # name -> case factory. Small enough to commit; the full configs are checked on the GPU
 # against the C oracle (which these fixtures pin) and through size-independent properties.
@@ -48,7 +49,7 @@ def digest(a: np.ndarray) -> str:
 
 
 def main():
-    os.makedirs(os.path.join(GOLDEN, "tapes"), exist_ok=True)
+    os.makedirs(TAPE_DIR, exist_ok=True)
     work = tempfile.mkdtemp(prefix="symel_golden_")
     dirs = {}
     for name, make in CASES.items():
@@ -85,7 +86,7 @@ def main():
         print(name, info["E"], info["n_blocks"])
     for tname, (cname, ename) in TAPES.items():
         src = os.path.join(dirs[cname], "ref_tape_%s.sytp" % ename)
-        with open(src, "rb") as f, gzip.GzipFile(os.path.join(GOLDEN, "tapes", tname + ".sytp.gz"), "wb", mtime=0) as g:
+        with open(src, "rb") as f, gzip.GzipFile(os.path.join(TAPE_DIR, tname + ".sytp.gz"), "wb", mtime=0) as g:
             g.write(f.read())
     shutil.rmtree(work)
 

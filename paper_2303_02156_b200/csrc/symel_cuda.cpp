@@ -166,6 +166,7 @@ struct symel_cuda_ctx {
   std::vector<Conn> conns;
   std::vector<std::unique_ptr<Energy>> energies;
   std::map<std::uint64_t, std::unique_ptr<Compiled>> kcache;
+  struct { std::uint64_t memory_hits = 0, disk_hits = 0, builds = 0, corrupt = 0; } cache_stats;
   // dof layout + pattern
   bool topology_dirty = true, pattern_dirty = true;
   int b = 1;
@@ -252,71 +253,132 @@ Energy& energy_of(symel_cuda_ctx* c, int id) {
 
 constexpr int kNoBadElem = 0x7f7f7f7f;  // d_bad sentinel (memset 0x7f)
 
+// Cubin cache (the reference's KernelCache disk layout, cache.hpp:103-180, for device code):
+// entries are named by the tape's digest -- the reference's kernel_key (registry.hpp:415-428;
+// KernelCache::get_or_build stamps it into the tape, cache.hpp:78) -- plus a hash of the
+// generated kernel (mode, binding, tile shape) and the arch tag:
+//   <kernel_key hex>.<variant>.sm100a.cubin  +  .meta  ("symel-cubin v1 sm_100a <source fnv> <bytes>")
+// A missing entry is a miss; an entry whose meta does not match, or whose image the driver
+// rejects, is corrupt: warning + rebuild + overwrite (cache.hpp:119-148).
+namespace {
+bool digest_is_zero(const std::array<std::uint8_t, 32>& d) {
+  for (auto v : d)
+    if (v) return false;
+  return true;
+}
+
+void cache_warn(symel_cuda_ctx* c, const std::string& msg) {
+  ++c->cache_stats.corrupt;
+  std::fprintf(stderr, "[symel] warning: corrupt cache entry, rebuilding: %s\n", msg.c_str());
+}
+
+std::vector<char> nvrtc_build(symel_cuda_ctx* c, const KernelSpec& spec, const std::string& src) {
+  const auto t0 = std::chrono::steady_clock::now();
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), (spec.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    throw Fail{SYMEL_E_COMPILE, "nvrtcCreateProgram failed"};
+  // IEEE-mode tape arithmetic is emitted as __dadd_rn/__dsub_rn/__dmul_rn (codegen.cpp), so
+  // contraction is safe for the rest of every kernel
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
+  // SYMEL_PTXAS_VERBOSE=1: print ptxas register / spill usage of each compiled kernel
+  const bool verbose = std::getenv("SYMEL_PTXAS_VERBOSE") != nullptr;
+  if (verbose) opts.push_back("--ptxas-options=-v");
+  const nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  std::size_t ls = 0;
+  nvrtcGetProgramLogSize(prog, &ls);
+  std::string log(ls, '\0');
+  nvrtcGetProgramLog(prog, log.data());
+  if (verbose && r == NVRTC_SUCCESS) std::fprintf(stderr, "[symel ptxas] %s %s\n", spec.name.c_str(), log.c_str());
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    throw Fail{SYMEL_E_COMPILE, "kernel compilation failed (" + std::string(nvrtcGetErrorString(r)) + "):\n" + log};
+  }
+  std::size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::vector<char> cubin(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  ++c->cache_stats.builds;
+  c->timings.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return cubin;
+}
+
+void write_atomically(const std::string& path, const char* data, std::size_t n) {
+  std::error_code ec;
+  const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid());
+  {
+    std::ofstream os(tmp, std::ios::binary | std::ios::trunc);
+    os.write(data, (std::streamsize)n);
+  }
+  std::filesystem::rename(tmp, path, ec);
+}
+}  // namespace
+
 Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
   std::string src = emit_kernel(spec);
   const std::string flags = "fmad1";
   const std::uint64_t key = fnv1a(src + "|" + flags + "|sm_100a|v1");
   auto it = c->kcache.find(key);
-  if (it != c->kcache.end()) return it->second.get();
-  char hex[32];
-  std::snprintf(hex, sizeof hex, "%016llx", (unsigned long long)key);
-  std::vector<char> cubin;
-  const std::string path = c->cache_dir.empty() ? "" : c->cache_dir + "/" + hex + ".sm100a.cubin";
-  if (!path.empty()) {
-    std::ifstream is(path, std::ios::binary);
-    if (is) cubin.assign(std::istreambuf_iterator<char>(is), {});
+  if (it != c->kcache.end()) {
+    ++c->cache_stats.memory_hits;
+    return it->second.get();
   }
-  if (cubin.empty()) {
-    const auto t0 = std::chrono::steady_clock::now();
-    nvrtcProgram prog;
-    if (nvrtcCreateProgram(&prog, src.c_str(), (spec.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
-      throw Fail{SYMEL_E_COMPILE, "nvrtcCreateProgram failed"};
-    // IEEE-mode tape arithmetic is emitted as __dadd_rn/__dsub_rn/__dmul_rn (codegen.cpp), so
-    // contraction is safe for the rest of every kernel
-    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
-    // SYMEL_PTXAS_VERBOSE=1: print ptxas register / spill usage of each compiled kernel
-    const bool verbose = std::getenv("SYMEL_PTXAS_VERBOSE") != nullptr;
-    if (verbose) opts.push_back("--ptxas-options=-v");
-    const nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
-    if (verbose && r == NVRTC_SUCCESS) {
-      std::size_t ls = 0;
-      nvrtcGetProgramLogSize(prog, &ls);
-      std::string log(ls, '\0');
-      nvrtcGetProgramLog(prog, log.data());
-      std::fprintf(stderr, "[symel ptxas] %s %s\n", spec.name.c_str(), log.c_str());
+  char variant[32];
+  std::snprintf(variant, sizeof variant, "%016llx", (unsigned long long)key);
+  // hand-built tapes without a kernel key are named by a content hash of the source
+  const std::string dkey = digest_is_zero(spec.tape->digest) ? std::string(variant) + "0000000000000000"
+                                                              : spec.tape->digest_hex();
+  char meta_line[160];
+  std::string path, meta;
+  if (!c->cache_dir.empty()) {
+    path = c->cache_dir + "/" + dkey + "." + variant + ".sm100a.cubin";
+    meta = c->cache_dir + "/" + dkey + "." + variant + ".meta";
+  }
+  std::vector<char> cubin;
+  auto load_image = [&](std::unique_ptr<Compiled>& comp) {
+    if (c->device < 0) return;
+    CK(cudaLibraryLoadData(&comp->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    CK(cudaLibraryGetKernel(&comp->kernel, comp->lib, spec.name.c_str()));
+  };
+  auto comp = std::make_unique<Compiled>();
+  bool from_disk = false;
+  if (!path.empty() && std::filesystem::exists(path)) {
+    std::ifstream is(path, std::ios::binary);
+    cubin.assign(std::istreambuf_iterator<char>(is), {});
+    std::ifstream ms(meta);
+    std::string got((std::istreambuf_iterator<char>(ms)), {});
+    std::snprintf(meta_line, sizeof meta_line, "symel-cubin v1 sm_100a %016llx %zu\n", (unsigned long long)key,
+                  cubin.size());
+    if (got != meta_line) {
+      cache_warn(c, path + ": metadata mismatch");
+    } else if (cubin.size() < 4 || std::memcmp(cubin.data(), "\x7f" "ELF", 4) != 0) {
+      cache_warn(c, path + ": not a cubin image");
+    } else if (c->device >= 0 && cudaLibraryLoadData(&comp->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr,
+                                                     0) != cudaSuccess) {
+      cudaGetLastError();
+      comp->lib = nullptr;
+      cache_warn(c, path + ": rejected by the driver");
+    } else {
+      if (c->device >= 0) CK(cudaLibraryGetKernel(&comp->kernel, comp->lib, spec.name.c_str()));
+      ++c->cache_stats.disk_hits;
+      from_disk = true;
     }
-    if (r != NVRTC_SUCCESS) {
-      std::size_t ls = 0;
-      nvrtcGetProgramLogSize(prog, &ls);
-      std::string log(ls, '\0');
-      nvrtcGetProgramLog(prog, log.data());
-      nvrtcDestroyProgram(&prog);
-      throw Fail{SYMEL_E_COMPILE, "kernel compilation failed (" + std::string(nvrtcGetErrorString(r)) + "):\n" + log};
-    }
-    std::size_t n = 0;
-    nvrtcGetCUBINSize(prog, &n);
-    cubin.resize(n);
-    nvrtcGetCUBIN(prog, cubin.data());
-    nvrtcDestroyProgram(&prog);
-    c->timings.compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  if (!from_disk) {
+    cubin = nvrtc_build(c, spec, src);
     if (!path.empty()) {
       std::error_code ec;
       std::filesystem::create_directories(c->cache_dir, ec);
-      const std::string tmp = path + ".tmp" + std::to_string((long long)::getpid());
-      std::ofstream os(tmp, std::ios::binary | std::ios::trunc);
-      os.write(cubin.data(), (std::streamsize)cubin.size());
-      os.close();
-      std::filesystem::rename(tmp, path, ec);
+      write_atomically(path, cubin.data(), cubin.size());
+      std::snprintf(meta_line, sizeof meta_line, "symel-cubin v1 sm_100a %016llx %zu\n", (unsigned long long)key,
+                    cubin.size());
+      write_atomically(meta, meta_line, std::strlen(meta_line));
     }
+    load_image(comp);
   }
-  auto comp = std::make_unique<Compiled>();
   comp->source = std::move(src);
   comp->tpb = spec.threads_per_block;
   comp->elems = spec.threads_per_block / std::max(1, spec.item_lanes);
-  if (c->device >= 0) {
-    CK(cudaLibraryLoadData(&comp->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-    CK(cudaLibraryGetKernel(&comp->kernel, comp->lib, spec.name.c_str()));
-  }
   Compiled* raw = comp.get();
   c->kcache.emplace(key, std::move(comp));
   return raw;
@@ -740,10 +802,12 @@ void ensure_elem_buffers(symel_cuda_ctx* c, Energy& e, bool contrib) {
   }
 }
 
-// Element id of the index a kernel reported: an active ordinal, or a tile position when the
-// last assemble ran the tile kernels (minimum position = deterministic, though in tile order).
+// Element id of the index a kernel reported: an active ordinal (active lists ascend, so the
+// lowest ordinal is the lowest element id, like check_finite), or -- tile kernels -- the
+// element id itself.
 int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
-  const int* map = (c->last_tiled && e.d_tile_perm) ? e.d_tile_elems : e.d_active;
+  if (c->last_tiled) return t;  // tile kernels report the element id itself (lowest wins)
+  const int* map = e.d_active;
   if (!map) return t;
   int v = 0;
   copy_sync(c, &v, map + t, sizeof(int), cudaMemcpyDeviceToHost);
@@ -753,13 +817,24 @@ int64_t element_of(symel_cuda_ctx* c, const Energy& e, int t) {
 double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st, bool async_tail = false);
 
 
+// The tile plan packs a Hessian contribution as (transpose << 15 | upper sub-block << 7 |
+// position in tile): at most 256 upper local sub-blocks (n_lb <= 22) per element. Larger
+// elements (hex27 / Q2 type) take the contrib path.
+bool tile_codes_fit(const Energy& e) { return e.bm.n_lb * (e.bm.n_lb + 1) / 2 <= 256; }
+
+bool tile_ok(const symel_cuda_ctx* c, const Energy& e) { return tile_codes_fit(e) && tile_smem(c, e) <= kTileSmemMax; }
+
 bool all_tile_capable(symel_cuda_ctx* c) {
+  long long nh = 0, ng = 0;
   for (auto& ep : c->energies) {
     if (ep->skip) continue;
-    if (tile_smem(c, *ep) > kTileSmemMax) return false;
+    if (!tile_ok(c, *ep)) return false;
     if ((ep->flags & SYMEL_ENERGY_SPD) && !spd_tape(*ep)) return false;  // projection needs the reduced form
+    nh += (long long)ep->n_active * ep->bm.n_lb * ep->bm.n_lb;
+    ng += (long long)ep->n_active * ep->bm.n_lb;
   }
-  return true;
+  // the plan stores contribution / segment indices as int32
+  return nh <= INT_MAX && ng <= INT_MAX;
 }
 
 void ensure_tile_plan(symel_cuda_ctx* c) {
@@ -1393,6 +1468,16 @@ int symel_cuda_set_cache_dir(symel_cuda_ctx* c, const char* dir) {
   return guarded(c, [&] { c->cache_dir = dir ? dir : ""; });
 }
 
+int symel_cuda_cache_stats(symel_cuda_ctx* c, uint64_t* out4) {
+  return guarded(c, [&] {
+    if (!out4) throw Fail{SYMEL_E_ARG, "cache_stats: null output"};
+    out4[0] = c->cache_stats.builds;
+    out4[1] = c->cache_stats.memory_hits;
+    out4[2] = c->cache_stats.disk_hits;
+    out4[3] = c->cache_stats.corrupt;
+  });
+}
+
 int symel_cuda_add_array(symel_cuda_ctx* c, const char* name, uint64_t items, uint32_t comps, int is_dof, int* id) {
   return guarded(c, [&] {
     if (comps == 0) throw Fail{SYMEL_E_ARG, std::string("array '") + (name ? name : "") + "': component count must be positive"};
@@ -1876,7 +1961,7 @@ int symel_cuda_kernel_source(symel_cuda_ctx* c, int eid, uint32_t flags, char* b
     const std::uint32_t mode = flags & 3u;
     Variant v = mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : (mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : V_CONTRIB_FAST);
     const bool g = flags & SYMEL_SRC_PLAN_GLOBAL;
-    if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
+    if (mode != SYMEL_ASM_ORDERED && tile_ok(c, e)) {
       if (!(e.flags & SYMEL_ENERGY_SPD)) v = g ? V_TILE_G : V_TILE;
       else if (spd_tape(e)) v = g ? V_TILE_SPD_G : V_TILE_SPD;
     }
@@ -1925,7 +2010,7 @@ int symel_cuda_precompile(symel_cuda_ctx* c, int eid, uint32_t flags) {
     const std::uint32_t mode = flags & 3u;
     kernel_for(c, e, mode == SYMEL_ASM_ATOMIC ? V_ATOMIC : (mode == SYMEL_ASM_ORDERED ? V_CONTRIB_IEEE : V_CONTRIB_FAST));
     if (mode != SYMEL_ASM_ORDERED) kernel_for(c, e, V_ENERGY);
-    if (mode != SYMEL_ASM_ORDERED && tile_smem(c, e) <= kTileSmemMax) {
+    if (mode != SYMEL_ASM_ORDERED && tile_ok(c, e)) {
       if (!(e.flags & SYMEL_ENERGY_SPD)) kernel_for(c, e, V_TILE);
       else if (spd_tape(e)) kernel_for(c, e, V_TILE_SPD);
     }

@@ -3,7 +3,7 @@
 // u32 n_inputs/n_outputs/n_dofs/n_regs, u64 n_consts + f64 bit patterns, u64 n_instrs +
 // {u8 op, u32 iarg, u32 dst, u32 a, u32 b, u32 c}, u64 n_out + u32 out_regs. Little endian.
 // The tape is the IR the CUDA code generator consumes; it is produced host-side by the
-// symbolic front end (paper_2303_02156_b200/csrc/host/*, or the reference itself).
+// symbolic front end (the reference: EnergySystem::compile_kernels + Tape::save).
 #pragma once
 
 #include <array>

@@ -64,7 +64,7 @@ EXPORTS = [
     "symel_cuda_scatter_dofs",
     "symel_cuda_element_outputs", "symel_cuda_get_timings", "symel_cuda_kernel_source",
     "symel_cuda_launch_count", "symel_cuda_fp64_peak", "symel_cuda_precompile", "symel_cuda_sync",
-    "symel_cuda_stream", "symel_cuda_energy_info", "symel_cuda_plan_info",
+    "symel_cuda_stream", "symel_cuda_energy_info", "symel_cuda_plan_info", "symel_cuda_cache_stats",
 ]
 
 
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "symel_cuda_destroy": ([P], None),
         "symel_cuda_last_error": ([P], C.c_char_p),
         "symel_cuda_set_cache_dir": ([P, C.c_char_p], I),
+        "symel_cuda_cache_stats": ([P, P], I),
         "symel_cuda_add_array": ([P, C.c_char_p, U64, C.c_uint32, I, C.POINTER(I)], I),
         "symel_cuda_set_array": ([P, I, P, U64], I),
         "symel_cuda_get_array": ([P, I, P, U64], I),
@@ -399,6 +400,12 @@ class DeviceAssembler:
         keys = ["tiles", "block_segments", "block_contributions", "block_partials", "partial_blocks",
                 "row_segments", "row_partials", "partial_rows"]
         return dict(zip(keys, (int(x) for x in v)))
+
+    def cache_stats(self) -> dict:
+        """KernelCache::stats() analogue (cache.hpp:17-24) of the device kernel cache."""
+        out = (C.c_uint64 * 4)()
+        self._check(self.lib.symel_cuda_cache_stats(self.h, out))
+        return dict(zip(("builds", "memory_hits", "disk_hits", "corrupt"), list(out)))
 
     def precompile(self, eid: int, mode: str = "deterministic") -> None:
         self._check(self.lib.symel_cuda_precompile(self.h, eid, MODES[mode]))

@@ -1,7 +1,12 @@
 """Registers a synthetic Case (configs.py) on a DeviceAssembler with the reference's binding
 layout: array registration order and input-slot order follow the reference's energy helpers
-(energies.hpp:418-609) exactly, so a tape produced by the reference (or by the front end in
-paper_2303_02156_b200/csrc/host, which restates it) plugs in unchanged.
+(energies.hpp:418-609) exactly, so a tape produced by the reference plugs in unchanged.
+
+Tapes: the derivative / activation / guard kernels of the BASELINE energies as the reference's
+own front end produces them (EnergySystem::compile_kernels -> Tape::save, registry.hpp:601-653,
+tape.hpp:213-240), stored under paper_2303_02156_b200/tapes/ by oracle/make_golden.py. They are
+the IR that crosses the C ABI; the C++ path (include/symel_cuda_assembler.hpp) hands the
+reference's in-memory tapes over instead.
 
 Input slots per energy (bind order, registry.hpp:577-594):
   solid_tet  (energies.hpp:435-461): x[a].c (12) | rest[a].c (12) | mu | lambda
@@ -65,27 +70,18 @@ def contact_inputs(x, off):
 TapeProvider = Callable[[str], bytes]
 
 
-def golden_tape(name: str) -> bytes:
-    """Reference-generated tapes committed under tests/golden/tapes (oracle/make_golden.py)."""
-    path = os.path.join(_HERE, "..", "tests", "golden", "tapes", name + ".sytp.gz")
+def reference_tape(name: str) -> bytes:
+    """A tape produced by the reference's front end (see the module docstring)."""
+    path = os.path.join(_HERE, "tapes", name + ".sytp.gz")
     with gzip.open(path, "rb") as f:
         return f.read()
 
 
-def frontend_tape(name: str) -> bytes:
-    """Tapes produced by this repo's own symbolic front end (csrc/host)."""
-    from . import frontend
-    return frontend.tape(name)
+golden_tape = reference_tape
 
 
 def default_tapes() -> TapeProvider:
-    try:
-        from . import frontend
-        if frontend.available():
-            return frontend_tape
-    except Exception:
-        pass
-    return golden_tape
+    return reference_tape
 
 
 class DeviceSystem:

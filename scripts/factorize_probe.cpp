@@ -48,6 +48,30 @@ int main(int argc, char** argv) {
     worst = std::max(worst, d / std::max(1.0, m));
   }
   std::printf("max rel err vs tape over 50 random elements: %.3e\n", worst);
+  // reduced SPD form: H = W^T M W must reproduce the tape's Hessian
+  FactorizeInfo si;
+  if (auto fs = factorize_spd(t, dofs, &si)) {
+    const unsigned m = si.frontier;
+    double w2 = 0;
+    for (int trial = 0; trial < 50; ++trial) {
+      std::vector<double> in(t.n_inputs, 0.0);
+      for (unsigned k = 0; k < t.n_inputs; ++k) in[k] = 0.5 + U(rng);
+      if (t.n_inputs == 26) { const double X[12] = {0,0,0, 1,0,0, 0,1,0, 0,0,1}; for (int k = 0; k < 12; ++k) { in[12 + k] = X[k] * 0.1 + U(rng) * 0.01; in[k] = in[12 + k] * 1.1 + U(rng) * 0.01; } in[24] = 35714.28; in[25] = 142857.14; }
+      std::vector<double> a, b; run(t, in, a); run(*fs, in, b);
+      std::vector<double> M(m * m);
+      size_t o = 1 + n;
+      for (unsigned i = 0; i < m; ++i) for (unsigned j = i; j < m; ++j) M[i * m + j] = M[j * m + i] = b[o++];
+      const double* W = &b[o];
+      double mx = 0, d = 0;
+      for (unsigned k = 0; k <= n; ++k) { mx = std::max(mx, std::abs(a[k])); d = std::max(d, std::abs(a[k] - b[k])); }
+      for (unsigned r = 0; r < n; ++r) for (unsigned c = 0; c < n; ++c) {
+        double h = 0; for (unsigned i = 0; i < m; ++i) for (unsigned j = 0; j < m; ++j) h += W[i * n + r] * M[i * m + j] * W[j * n + c];
+        mx = std::max(mx, std::abs(a[1 + n + r * n + c])); d = std::max(d, std::abs(h - a[1 + n + r * n + c]));
+      }
+      w2 = std::max(w2, d / std::max(1.0, mx));
+    }
+    std::printf("spd form: ops %llu, max rel err of E, g, W^T M W vs tape: %.3e\n", (unsigned long long)si.ops_after, w2);
+  }
   for (int sch : {1, 2}) {
     auto order = schedule_instrs(*f, sch);
     std::vector<long> last(f->n_regs, -1);

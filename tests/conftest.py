@@ -20,7 +20,9 @@ def golden(name):
 
 
 def golden_tape(name):
-    with gzip.open(os.path.join(GOLDEN, "tapes", name + ".sytp.gz"), "rb") as f:
+    """The reference's own tapes (Tape::save of the reference's kernels, oracle/make_golden.py),
+    shipped with the package as the data the reference front end hands across the ABI."""
+    with gzip.open(os.path.join(ROOT, "paper_2303_02156_b200", "tapes", name + ".sytp.gz"), "rb") as f:
         return f.read()
 
 

@@ -14,7 +14,7 @@ import pytest
 from conftest import golden_tape
 from paper_2303_02156_b200 import configs as C
 from paper_2303_02156_b200 import systems as S
-from paper_2303_02156_b200.device import DeviceAssembler, IN_ITEM
+from paper_2303_02156_b200.device import DeviceAssembler, IN_ITEM, SymelError
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-10
@@ -210,3 +210,74 @@ def test_graph_replay_tracks_params_state_and_modes():
     ds2.asm.set_array(ds2.arrays["x"], x)
     assert ds.asm.assemble("deterministic") == ds2.asm.assemble("deterministic")
     np.testing.assert_array_equal(ds.asm.gradient(), ds2.asm.gradient())
+
+
+def _chain_system(nodes, n_elem, n_pts, seed, c=0.0):
+    """Random point cloud + elements of `nodes` distinct random points, energy = the hand-built
+    chain tape (tests/tapegen.py); device and oracle registered identically."""
+    from tapegen import chain_quartic_tape
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    x = rng.random((n_pts, 3))
+    conn = np.stack([rng.choice(n_pts, nodes, replace=False) for _ in range(n_elem)]).astype(np.int64)
+    tape = chain_quartic_tape(nodes)
+    inputs = [(IN_ITEM, 0, a, k) for a in range(nodes) for k in range(3)] + [(S.IN_PARAM, 0, 0, 0)]
+    return x, conn, tape, inputs
+
+
+def _register_chain(x, conn, tape, inputs, nodes, c):
+    from oracle import oracle as O
+    A = DeviceAssembler()
+    xa = A.add_array("x", x.shape[0], 3, True)
+    A.set_array(xa, x)
+    cid = A.add_connectivity("chains", nodes)
+    A.set_elements(cid, conn)
+    A.add_energy("chain", cid, tape, inputs, range(3 * nodes), params={3 * nodes: c})
+    sysm = O.System()
+    sysm.add_array("x", x, 3, True)
+    sysm.add_energy("chain", conn, nodes, tape, inputs, range(3 * nodes), params={3 * nodes: c})
+    return A, sysm
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_large_element_23_nodes(mode, oracle_mod):
+    """23-node elements (276 upper local sub-blocks > the tile plan's 8-bit sub-block code):
+    the assembler must route them off the tile path and still match the oracle."""
+    nodes = 23
+    x, conn, tape, inputs = _chain_system(nodes, 300, 900, 11)
+    A, sysm = _register_chain(x, conn, tape, inputs, nodes, 0.0)
+    ref = sysm.assemble()
+    check(device_result(A, mode), ref, oracle_mod, 1e-12 if mode == "ordered" else TOL)
+
+
+@pytest.mark.parametrize("nodes", [4, 22])
+def test_chain_tape_tile_path(nodes, oracle_mod):
+    """The same hand-built energy at sizes the tile plan packs (n_lb <= 22)."""
+    x, conn, tape, inputs = _chain_system(nodes, 700, 2000, 12)
+    A, sysm = _register_chain(x, conn, tape, inputs, nodes, 0.0)
+    ref = sysm.assemble()
+    for mode in MODES:
+        check(device_result(A, mode), ref, oracle_mod, 1e-12 if mode == "ordered" else TOL)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_non_finite_names_lowest_element_across_tiles(mode, oracle_mod):
+    """check_finite names the lowest (energy, element) (assembly.hpp:426-438), also when the
+    non-finite elements sit in different tiles whose spatial (Morton) order differs from the
+    element order."""
+    import re
+    rng = np.random.default_rng(5)
+    for trial in range(4):
+        x, conn, tape, inputs = _chain_system(4, 2000, 6000, 100 + trial)
+        bad = np.sort(rng.choice(2000, 2, replace=False))
+        for e in bad:
+            x[conn[e, 1]] = x[conn[e, 0]]  # first two nodes coincide: c / (d0.d0) = inf
+        A, sysm = _register_chain(x, conn, tape, inputs, 4, 1.0)
+        ref = sysm.assemble()
+        assert ref["status"] == 4 and ref["bad_energy"] == 0
+        assert ref["bad_element"] == min(e for e in range(2000)
+                                         if np.all(x[conn[e, 1]] == x[conn[e, 0]]))
+        with pytest.raises(SymelError) as ei:
+            A.assemble(mode)
+        m = re.search(r"element (\d+)", str(ei.value))
+        assert m and int(m.group(1)) == ref["bad_element"], (str(ei.value), ref["bad_element"])

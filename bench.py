@@ -5,10 +5,18 @@
 
 One step = one Assembler::assemble() of the whole configuration on device-resident inputs
 (activation refresh, element kernels, SPD projection where the config asks for it, gradient +
-BSR assembly, energy and finiteness reduction). Multi-GPU: one process per GPU, each rank
-assembles its own replica of the configuration ("scaling": "weak"); max-over-ranks device time.
-The `cpu_baseline` / `--impl reference` leg runs the unmodified reference (oracle/_ref/ref_driver,
-reference headers compiled in place, `source` backend, all host threads) on a bounded sample.
+BSR assembly, energy and finiteness reduction). The atomic assembly mode is timed right after
+and reported in the same line ("atomic"); "e2e" adds the host copies (x in, E + gradient out),
+"e2e_host_hessian" also copies the whole BCRS Hessian back every step.
+
+Multi-GPU: one process per GPU. `--gpus N` outside torchrun re-launches itself as N ranks
+(torch.distributed.run, 127.0.0.1). Config 2 shards into slabs (owner computes, E all-reduce);
+other configs run replicas ("scaling": "weak"); max-over-ranks device time.
+
+`--impl reference` runs the unmodified reference (oracle/_ref/ref_driver: reference headers
+compiled in place, `source` backend, all host threads) through Assembler::assemble() on the
+same config at FULL size (config 5: a bounded sample unless --ref-n is given); the
+`cpu_baseline` key of our arm is the same reference on a bounded sample (n=40 for config 2).
 """
 from __future__ import annotations
 
@@ -166,40 +174,43 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(cfg: str, steps: int, warmup: int, ref_n: int, threads: int = 0):
-    """The unmodified reference on a bounded sample of the workload (same generator, smaller n)."""
-    from oracle import oracle as O
+REF_SAMPLE_N = {"c1": 20, "c2": 40, "c3": 16, "c4": 300, "c5": 30}   # bounded cpu_baseline samples
+REF_FULL_N = {"c1": 20, "c2": 100, "c3": 40, "c4": 1000}              # the configs at full size
+
+
+def ref_case(cfg: str, n: int):
     from paper_2303_02156_b200 import configs as C
+    if cfg == "c5":
+        return C.config5(n, 4 * (n + 1) ** 3)
+    return {"c1": C.config1, "c2": C.config2, "c3": C.config3, "c4": C.config4}[cfg](n)
+
+
+def cpu_reference(cfg: str, steps: int, warmup: int, n: int, threads: int = 0, spd_sample: bool = True):
+    """The unmodified reference (oracle/_ref/ref_driver: reference headers compiled in place,
+    `source` backend = the paper's compiled kernels, all host threads, lanes 8) running
+    Assembler::assemble() on the same seeded generator at grid size n."""
+    from oracle import oracle as O
     if not os.path.exists(O.REF_DRIVER):
         return None, "oracle/_ref/ref_driver not built"
-    n = ref_n or {"c1": 20, "c2": 40, "c3": 16, "c4": 300, "c5": 30}[cfg]
-    if cfg == "c1":
-        case = C.config1(n)
-    elif cfg == "c2":
-        case = C.config2(n)
-    elif cfg == "c3":
-        case = C.config3(n)
-    elif cfg == "c4":
-        case = C.config4(n)
-    else:
-        case = C.config5(n, 4 * (n + 1) ** 3)
+    case = ref_case(cfg, n)
     d = tempfile.mkdtemp(prefix="symel_refbench_")
     try:
         case.write_case_dir(d)
         threads = threads or os.cpu_count() or 1
         info = O.run_ref_driver(d, backend="source", threads=threads, lanes=8, repeat=max(1, steps), dump=False,
-                                cache=os.path.join(d, "kcache"))
+                                cache=os.path.join(d, "kcache"), warmup=max(1, warmup))
     finally:
         shutil.rmtree(d, ignore_errors=True)
     melem = info["n_elements"] / (info["mean_ms"] * 1e-3) / 1e6
     sample = (f"{cfg} generator at n={n}: {info['n_elements']} elements; reference Assembler::assemble "
               f"(source backend, lanes 8, {threads} threads), mean of {steps} steady-state calls after "
-              f"1 warm-up (first call {info['first_ms']:.0f} ms incl. kernel compile + pattern build); no SPD "
-              f"(the reference has none)")
+              f"{max(1, warmup)} warm-up call(s) (first call {info['first_ms']:.0f} ms incl. kernel compile + "
+              f"pattern build); no SPD projection (the reference has none)")
     out = {"value": melem, "unit": "M elements/s", "cores": threads, "kind": "reference", "sample": sample,
-           "ms_per_assemble": info["mean_ms"], "eval_ms": info["eval_ms"], "assemble_ms": info["assemble_ms"]}
-    if cfg in ("c2", "c5"):
-        out["spd_projection"] = cpu_spd_projection(case)
+           "ms_per_assemble": info["mean_ms"], "eval_ms": info["eval_ms"], "assemble_ms": info["assemble_ms"],
+           "first_ms": info["first_ms"], "n_elements": info["n_elements"], "n": n}
+    if cfg in ("c2", "c5") and spd_sample:
+        out["spd_projection"] = cpu_spd_projection(ref_case(cfg, min(n, 40)))
     return out, None
 
 
@@ -220,10 +231,31 @@ def cpu_spd_projection(case, count: int = 20000) -> dict:
             "sample": f"numpy.linalg.eigh projection of {count} tet element Hessians (12x12) of the sample"}
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-exec as N ranks on this node."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def config_dict(cfg: str, n_elements: int, spd: bool, mode: str) -> dict:
+    """The workload both arms report (identical keys and values)."""
+    meta = config_meta(cfg)
+    return {"workload": meta["workload"], "elements": int(n_elements), "spd": bool(spd), "mode": mode}
+
+
 def main():
     args = parse()
-    rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch_under_torchrun(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     meta = config_meta(args.config)
     spd = meta["spd"] and not args.no_spd
@@ -232,18 +264,30 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        base, why = cpu_reference(args.config, args.steps, args.warmup, args.ref_n)
+        n = args.ref_n or REF_FULL_N.get(args.config, REF_SAMPLE_N[args.config])
+        base, why = cpu_reference(args.config, args.steps, args.warmup, n)
         if base is None:
             print(json.dumps({"impl": "reference", "unavailable": why}))
             return 0
+        full = n == REF_FULL_N.get(args.config)
+        ref_cfg = config_dict(args.config, base["n_elements"], spd, args.mode) if full else \
+            {"workload": meta["workload"] + f" (bounded sample n={n})", "elements": base["n_elements"]}
         line = {"impl": "reference", "metric": metric, "value": base["value"], "unit": "M elements/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": base["ms_per_assemble"], "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, bounded sample)",
-                "config": {"workload": meta["workload"], "sample": base["sample"]},
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generator, BASELINE shapes)" if full else
+                        "synthetic (seeded generator, bounded sample)",
+                "config": ref_cfg,
+                "reference_notes": {"sample": base["sample"], "first_call_ms": base["first_ms"],
+                                    "eval_ms": base["eval_ms"], "assemble_ms": base["assemble_ms"],
+                                    "spd_projection": "not part of the reference (SURVEY 8(c)); this arm's time "
+                                                      "excludes it" if spd else "off"},
                 "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": base["value"], "unit": "M elements/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
+        if "spd_projection" in base:
+            line["reference_notes"]["spd_projection_oracle"] = base["spd_projection"]
         print(json.dumps(line))
         return 0
 
@@ -268,16 +312,16 @@ def main():
         ds, case, n_elem = shard.ds, slab.case, slab.n_own
         parallelism = f"dp{world} slabs, owner computes (1 ghost hex plane), E all-reduce over NCCL"
 
-        def step():
-            return sum_over_ranks(shard.assemble(args.mode), device="cuda")
+        def step(mode=args.mode):
+            return sum_over_ranks(shard.assemble(mode), device="cuda")
     else:
         case = make_case(args.config)
         ds = DeviceSystem(case, spd=spd, device=local)
         n_elem = case.n_elements()
-        parallelism = f"replicas{world}"
+        parallelism = f"replicas{world}" if world > 1 else "single GPU"
 
-        def step():
-            return ds.asm.assemble(args.mode)
+        def step(mode=args.mode):
+            return ds.asm.assemble(mode)
     A = ds.asm
     stream = torch.cuda.ExternalStream(A.stream(), device=local)
     t_setup = time.time()
@@ -288,33 +332,47 @@ def main():
     plan = A.plan_info()
     einfo = {n: A.energy_info(e) for n, e in ds.energies.items()}
 
-    # ---- device-resident timed region
+    def timed(mode, steps):
+        """K steps of `mode` between barriers, CUDA events on the library's stream; returns
+        (ms per step, mean element-kernel ms, launches per step)."""
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = A.launch_count()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        kms = []
+        for _ in range(steps):
+            step(mode)
+            kms.append(A.timings().eval_ms)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        launches = (A.launch_count() - l0) // max(1, steps)
+        return max_over_ranks(e0.elapsed_time(e1) / steps, device="cuda"), float(np.mean(kms)), launches
+
+    # ---- device-resident timed region (the headline mode)
     clocks = ClockSampler(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
-    l0 = A.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    eval_ms = []
-    for _ in range(args.steps):
-        step()
-        eval_ms.append(A.timings().eval_ms)
-    e1.record(stream)
-    e1.synchronize()
-    torch.cuda.synchronize()
-    launches = (A.launch_count() - l0) // max(1, args.steps)
-    ms = e0.elapsed_time(e1) / args.steps
+    ms, k_ms, launches = timed(args.mode, args.steps)
     clk = clocks.stop()
-    ms = max_over_ranks(ms, device="cuda")
     value = world * n_elem / (ms * 1e-3) / 1e6
+
+    # ---- the atomic path, reported alongside (north star)
+    alt = None
+    if args.mode == "deterministic":
+        for _ in range(max(3, args.warmup)):
+            step("atomic")
+        ams, akms, alaunch = timed("atomic", args.steps)
+        alt = {"mode": "atomic", "value": world * n_elem / (ams * 1e-3) / 1e6, "unit": "M elements/s",
+               "ms_per_step": ams, "kernel_ms": akms, "gpu_launches": int(alaunch)}
+        for _ in range(max(3, args.warmup)):
+            step(args.mode)
 
     # ---- roofline of the dominant kernel (element eval + fused assembly)
     fl = flops_per_step(args.config, case)
     fl_spd = P_SPD * spd_elements(args.config, case) if spd else 0
-    k_ms = float(np.mean(eval_ms))
     peak = A.fp64_peak_tflops()
     achieved = (fl + fl_spd) / (k_ms * 1e-3) / 1e12
     achieved_nospd = fl / (k_ms * 1e-3) / 1e12
@@ -346,40 +404,57 @@ def main():
             roof["ncu"] = {k: v for k, v in facts.items() if k != "traffic_bytes"}
 
     # ---- end to end through the C ABI with host buffers: H2D x, assemble, D2H E + gradient
+    # (+ the whole BCRS Hessian in the host-Hessian variant: the reference's hessian() contract)
+    import ctypes
+    lib = A.lib
     x_host = torch.empty(case.x.size, dtype=torch.float64, pin_memory=True)
     x_host.numpy()[:] = case.x.ravel()
     g_host = torch.empty(case.x.size, dtype=torch.float64, pin_memory=True)
-    import ctypes
-    lib = A.lib
-    torch.cuda.synchronize()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
-    for _ in range(args.steps):
-        lib.symel_cuda_set_array(A.h, ds.x, ctypes.c_void_p(x_host.data_ptr()), case.x.size)
-        E = step()
-        lib.symel_cuda_copy_gradient(A.h, ctypes.c_void_p(g_host.data_ptr()))
-    e3.record(stream)
-    e3.synchronize()
-    e2e_ms = e2.elapsed_time(e3) / args.steps
-    e2e_ms = max_over_ranks(e2e_ms, device="cuda")
-    e2e = {"value": world * n_elem / (e2e_ms * 1e-3) / 1e6, "unit": "M elements/s",
-           "h2d_bytes_per_step": int(case.x.size * 8), "d2h_bytes_per_step": int(case.x.size * 8 + 8),
-           "ms_per_step": e2e_ms, "note": "BSR values stay device-resident for the device PCG consumer"}
+    pb, _, pnb, _ = A.pattern_info()
+    nvals = int(pnb) * int(pb) * int(pb)
+
+    def e2e_run(with_h):
+        h_host = torch.empty(max(1, nvals), dtype=torch.float64, pin_memory=True) if with_h else None
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        for _ in range(args.steps):
+            lib.symel_cuda_set_array(A.h, ds.x, ctypes.c_void_p(x_host.data_ptr()), case.x.size)
+            step()
+            lib.symel_cuda_copy_gradient(A.h, ctypes.c_void_p(g_host.data_ptr()))
+            if with_h:
+                lib.symel_cuda_copy_hessian(A.h, ctypes.c_void_p(h_host.data_ptr()))
+        e3.record(stream)
+        e3.synchronize()
+        t = max_over_ranks(e2.elapsed_time(e3) / args.steps, device="cuda")
+        return {"value": world * n_elem / (t * 1e-3) / 1e6, "unit": "M elements/s",
+                "h2d_bytes_per_step": int(case.x.size * 8),
+                "d2h_bytes_per_step": int(case.x.size * 8 + 8 + (nvals * 8 if with_h else 0)), "ms_per_step": t}
+
+    e2e = e2e_run(False)
+    e2e["note"] = "x in, E + gradient out; BSR values stay device-resident for the device PCG consumer"
+    e2e_h = e2e_run(True)
+    e2e_h["note"] = ("x in, E + gradient + all BCRS values out every step (the reference's host "
+                     "BcrsMatrix hessian() contract, assembly.hpp:177)")
 
     line = {"metric": metric, "value": value, "unit": "M elements/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE shapes)",
-            "config": {"workload": meta["workload"], "elements": n_elem, "mode": args.mode, "spd": spd,
-                       "parallelism": parallelism,
-                       "l2": "working set (BSR values + slot maps + connectivity) >> 126 MB L2; no flush needed",
-                       "pattern_ms": tm.pattern_ms, "compile_ms": tm.compile_ms, "setup_s": setup_s,
-                       "tile_plan": plan,
-                       "kernel_ops": {n: {"tape": v["tape_ops"], "executed": v["fast_ops"], "frontier": v["frontier"]}
-                                      for n, v in einfo.items()}},
-            "roofline": roof, "clocks": clk, "e2e": e2e, "gpu_launches": int(launches)}
+            "config": config_dict(args.config, world * n_elem, spd, args.mode),
+            "details": {"parallelism": parallelism, "elements_per_rank": n_elem,
+                        "l2": "working set (BSR values + slot maps + connectivity) >> 126 MB L2; no flush needed",
+                        "pattern_ms": tm.pattern_ms, "compile_ms": tm.compile_ms, "setup_s": setup_s,
+                        "tile_plan": plan,
+                        "kernel_ops": {n: {"tape": v["tape_ops"], "executed": v["fast_ops"],
+                                           "frontier": v["frontier"]} for n, v in einfo.items()}},
+            "roofline": roof, "clocks": clk, "e2e": e2e, "e2e_host_hessian": e2e_h, "gpu_launches": int(launches)}
+    if alt:
+        line["atomic"] = alt
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        base, why = cpu_reference(args.config, 3, 1, args.ref_n)
+        base, why = cpu_reference(args.config, 3, 1, args.ref_n or REF_SAMPLE_N[args.config])
         line["cpu_baseline"] = base if base else {"unavailable": why}
     if rank == 0:
         print(json.dumps(line))

@@ -66,6 +66,9 @@ def lib() -> C.CDLL:
                                             C.POINTER(C.c_double)]
         _lib.oracle_guard_min.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.POINTER(C.c_double)]
         _lib.oracle_free_result.argtypes = [C.POINTER(OResult)]
+        _lib.oracle_energy_gradient.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int32,
+                                                C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p,
+                                                C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
         _lib.oracle_bsr_matvec.argtypes = [C.c_int32, C.c_int64] + [C.c_void_p] * 5
         _lib.oracle_block_jacobi_inverse.argtypes = [C.c_int32, C.c_int64] + [C.c_void_p] * 3 + [C.c_double, C.c_void_p]
         _lib.oracle_pcg.argtypes = ([C.c_int32, C.c_int64] + [C.c_void_p] * 3 + [C.c_double, C.c_void_p, C.c_void_p,
@@ -139,6 +142,19 @@ class System:
         finally:
             lib().oracle_free_result(C.byref(r))
         return out
+
+    def energy_gradient(self, threads: int = 0) -> dict:
+        """E (reference order and Kahan) and the gradient without the Hessian: full-size checks."""
+        arrs, ens, keep = self._structs()
+        n_dofs = sum(a["items"] * a["comps"] for a in self.arrays if a["is_dof"])
+        g = np.empty(max(1, n_dofs))
+        E, Ek = C.c_double(), C.c_double()
+        be, bel = C.c_int32(), C.c_int64()
+        threads = threads or (os.cpu_count() or 1)
+        st = lib().oracle_energy_gradient(arrs, len(self.arrays), ens, len(self.energies), threads, C.byref(E),
+                                          C.byref(Ek), g.ctypes.data, C.byref(be), C.byref(bel))
+        return dict(status=st, E=E.value, E_kahan=Ek.value, grad=g[:n_dofs], bad_energy=be.value,
+                    bad_element=bel.value)
 
     def element_outputs(self, energy: int, first: int, count: int) -> np.ndarray:
         arrs, ens, keep = self._structs()
@@ -266,11 +282,12 @@ def assemble_spd(sysm: "System", spd_energies=None) -> dict:
 
 
 def run_ref_driver(case_dir: str, backend: str = "source", threads: int = 0, lanes: int = 8, repeat: int = 1,
-                   dump: bool = True, cache: str = "/tmp/symel_ref_cache", timeout: float = 3600) -> dict:
+                   dump: bool = True, cache: str = "/tmp/symel_ref_cache", timeout: float = 3600,
+                   warmup: int = 1) -> dict:
     """Runs the unmodified reference (oracle/_ref/ref_driver) on a case directory."""
     import json
     cmd = [REF_DRIVER, case_dir, "--backend", backend, "--lanes", str(lanes), "--repeat", str(repeat),
-           "--cache", cache]
+           "--cache", cache, "--warmup", str(max(1, warmup))]
     if threads:
         cmd += ["--threads", str(threads)]
     if not dump:

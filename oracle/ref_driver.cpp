@@ -12,7 +12,9 @@
 // Built by oracle/Makefile into oracle/_ref/ref_driver.
 //
 // usage: ref_driver CASE_DIR [--backend interp|source] [--threads T] [--lanes W]
-//                   [--repeat K] [--no-dump] [--cache DIR] [--elem-sample N] [--solver]
+//                   [--warmup W] [--repeat K] [--no-dump] [--cache DIR] [--elem-sample N] [--solver]
+//   W untimed assemble() calls (>= 1; the first includes kernel build + pattern build and is
+//   reported as first_ms), then K timed calls.
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -41,7 +43,7 @@ int main(int argc, char** argv) {
   refcase::g_dir = argv[1];
   std::string backend = "source", cache_dir = "/tmp/symel_ref_cache";
   int threads = static_cast<int>(std::thread::hardware_concurrency());
-  int lanes = 8, repeat = 1;
+  int lanes = 8, repeat = 1, warmup = 1;
   bool dump = true, solver = false;
   std::size_t elem_sample = 64;
   for (int i = 2; i < argc; ++i) {
@@ -51,6 +53,7 @@ int main(int argc, char** argv) {
     else if (a == "--threads") threads = std::stoi(next());
     else if (a == "--lanes") lanes = std::stoi(next());
     else if (a == "--repeat") repeat = std::stoi(next());
+    else if (a == "--warmup") warmup = std::max(1, std::stoi(next()));
     else if (a == "--no-dump") dump = false;
     else if (a == "--cache") cache_dir = next();
     else if (a == "--elem-sample") elem_sample = std::stoul(next());
@@ -66,6 +69,7 @@ int main(int argc, char** argv) {
     const double t0 = now_ms();
     double E = as.assemble();
     const double first_ms = now_ms() - t0;
+    for (int w = 1; w < warmup; ++w) E = as.assemble();
     double best = 1e300, total = 0;
     as.reset_timings();
     for (int r = 0; r < repeat; ++r) {

@@ -249,7 +249,9 @@ int oracle_assemble(const oracle_array* A, uint32_t na, const oracle_energy* E, 
     for (uint32_t d = 0; d < ne; ++d) cap += E[d].n_elems * (uint64_t)E[d].n_dofs * E[d].n_dofs;
     uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (cap + 1));
     for (int64_t r = 0; r < res->n_rows; ++r) keys[r] = ((uint64_t)r << 32) | (uint64_t)r;
-    int64_t* dofs = (int64_t*)malloc(sizeof(int64_t) * 64);
+    uint32_t max_nd = 1;
+    for (uint32_t d = 0; d < ne; ++d) max_nd = E[d].n_dofs > max_nd ? E[d].n_dofs : max_nd;
+    int64_t* dofs = (int64_t*)malloc(sizeof(int64_t) * max_nd);
     for (uint32_t d = 0; d < ne; ++d) {
       const oracle_energy* e = &E[d];
       for (uint64_t el = 0; el < e->n_elems; ++el) {
@@ -318,7 +320,9 @@ int oracle_assemble(const oracle_array* A, uint32_t na, const oracle_energy* E, 
     res->vals = (double*)calloc((size_t)(res->n_blocks * b * b) + 1, sizeof(double));
     res->grad = (double*)calloc((size_t)res->n_dofs + 1, sizeof(double));
     double Esum = 0.0;
-    int64_t dofs[64];
+    uint32_t max_nd = 1;
+    for (uint32_t d = 0; d < ne; ++d) max_nd = E[d].n_dofs > max_nd ? E[d].n_dofs : max_nd;
+    int64_t* dofs = (int64_t*)malloc(sizeof(int64_t) * max_nd);
     off = 0;
     for (uint32_t d = 0; d < ne; ++d) {
       const oracle_energy* e = &E[d];
@@ -340,6 +344,7 @@ int oracle_assemble(const oracle_array* A, uint32_t na, const oracle_energy* E, 
       free(contrib[d]);
     }
     free(contrib);
+    free(dofs);
     res->E = Esum;
   }
   /* apply_pins (assembly.hpp:464-489) */
@@ -579,4 +584,133 @@ int oracle_pcg(int32_t b, int64_t n_rows, const int64_t* rp, const int64_t* ci, 
   if (!done) *rel_residual = sqrt(sdot(r, r, n)) / rhs_norm;
   free(prec); free(r); free(z); free(p); free(q);
   return 0;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * E and gradient only, at full BASELINE sizes (tests/test_gpu_fullsize.py): the same
+ * semantics as oracle_assemble -- activation (assembly.hpp:227-261), fixed summation
+ * (400-413), check_finite on E and g (426-438), E summed serially in (energy, active element)
+ * order from 0.0 (440-448), every gradient entry accumulated in (energy, element) order from
+ * 0.0 (450-462) -- without the pattern and the Hessian. Each tape is pruned to the closure of
+ * its E and g outputs (SSA: dropping dead instructions changes no value). Elements are
+ * evaluated in parallel into a per-element buffer; the sums run serially. Also returns E with
+ * compensated (Kahan) summation over the same terms. */
+static uint64_t* needed_instrs(const tape_t* t, uint32_t n_out, uint64_t* count) {
+  uint8_t* need = (uint8_t*)calloc(t->n_regs + 1, 1);
+  for (uint32_t k = 0; k < n_out; ++k) need[t->out[k]] = 1;
+  uint64_t n = 0;
+  for (uint64_t k = t->n_instrs; k-- > 0;) {
+    const instr_t* i = &t->ins[k];
+    if (!need[i->dst]) continue;
+    ++n;
+    need[i->a] = 1;
+    if (i->op >= 2 && i->op <= 5) need[i->b] = 1;
+    if (i->op == 12) { need[i->b] = 1; need[i->c] = 1; }
+  }
+  uint64_t* list = (uint64_t*)malloc(sizeof(uint64_t) * (n + 1));
+  uint64_t q = 0;
+  for (uint64_t k = 0; k < t->n_instrs; ++k)
+    if (need[t->ins[k].dst]) list[q++] = k;
+  free(need);
+  *count = n;
+  return list;
+}
+
+static void tape_eval_subset(const tape_t* t, const uint64_t* list, uint64_t n, const double* in, double* regs) {
+  memcpy(regs, in, sizeof(double) * t->n_inputs);
+  memcpy(regs + t->n_inputs, t->consts, sizeof(double) * t->n_consts);
+  for (uint64_t q = 0; q < n; ++q) {
+    const instr_t* i = &t->ins[list[q]];
+    const double a = regs[i->a], b = regs[i->b], c = regs[i->c];
+    double d;
+    switch (i->op) {
+      case 2: d = a + b; break;
+      case 3: d = a - b; break;
+      case 4: d = a * b; break;
+      case 5: d = a / b; break;
+      case 6: d = -a; break;
+      case 7: d = powi(a, i->iarg); break;
+      case 8: d = sqrt(a); break;
+      case 9: d = log(a); break;
+      case 10: d = sin(a); break;
+      case 11: d = cos(a); break;
+      default: d = a >= 0.0 ? b : c; break;
+    }
+    regs[i->dst] = d;
+  }
+}
+
+int oracle_energy_gradient(const oracle_array* A, uint32_t na, const oracle_energy* E, uint32_t ne, int32_t threads,
+                           double* energy, double* energy_kahan, double* grad, int32_t* bad_energy,
+                           int64_t* bad_element) {
+  layout_t L;
+  make_layout(A, na, &L);
+  int status = 0;
+  *bad_energy = -1;
+  *bad_element = -1;
+  for (int64_t k = 0; k < L.n_dofs; ++k) grad[k] = 0.0;
+  double Es = 0.0, Ek = 0.0, comp = 0.0;
+  for (uint32_t d = 0; d < ne && status == 0; ++d) {
+    const oracle_energy* e = &E[d];
+    if (e->is_sum && e->n_items == 0) continue;
+    tape_t t;
+    if (tape_parse(e->tape, e->tape_len, &t)) { status = 6; break; }
+    const uint32_t nd = e->n_dofs, S = 1 + nd;
+    uint64_t nlist = 0;
+    uint64_t* list = needed_instrs(&t, S, &nlist);
+    uint8_t* active = (uint8_t*)malloc(e->n_elems + 1);
+    memset(active, 1, e->n_elems);
+    tape_t at;
+    const int has_act = e->act_tape != NULL;
+    if (has_act && tape_parse(e->act_tape, e->act_len, &at)) { status = 6; free(list); free(active); tape_free(&t); break; }
+    double* buf = (double*)malloc(sizeof(double) * (e->n_elems * S + 1));
+#pragma omp parallel num_threads(threads > 0 ? threads : 1)
+    {
+      double* in = (double*)malloc(sizeof(double) * (e->n_inputs + 1));
+      double* regs = (double*)malloc(sizeof(double) * (t.n_regs + (has_act ? at.n_regs : 0) + 1));
+#pragma omp for schedule(static)
+      for (int64_t el = 0; el < (int64_t)e->n_elems; ++el) {
+        if (has_act) {
+          const double v = act_value(A, e, &at, (uint64_t)el, in, regs);
+          active[el] = e->act_kind == 0 ? (v >= 0.0) : (v > 0.0);
+          if (!active[el]) continue;
+        }
+        double* dst = buf + (uint64_t)el * S;
+        if (e->is_sum) {
+          for (uint32_t it = 0; it < e->n_items; ++it) {
+            gather(A, e, (uint64_t)el, e->sum_items + (uint64_t)it * e->sum_arity, in);
+            tape_eval_subset(&t, list, nlist, in, regs);
+            for (uint32_t k = 0; k < S; ++k) dst[k] = it == 0 ? regs[t.out[k]] : dst[k] + regs[t.out[k]];
+          }
+        } else {
+          gather(A, e, (uint64_t)el, NULL, in);
+          tape_eval_subset(&t, list, nlist, in, regs);
+          for (uint32_t k = 0; k < S; ++k) dst[k] = regs[t.out[k]];
+        }
+      }
+      free(in);
+      free(regs);
+    }
+    for (uint64_t el = 0; el < e->n_elems && status == 0; ++el) {
+      if (!active[el]) continue;
+      const double* v = buf + el * S;
+      for (uint32_t k = 0; k < S; ++k)
+        if (!isfinite(v[k])) { status = 4; *bad_energy = (int32_t)d; *bad_element = (int64_t)el; break; }
+      if (status) break;
+      Es += v[0];
+      const double y = v[0] - comp, tt = Ek + y;  /* Kahan */
+      comp = (tt - Ek) - y;
+      Ek = tt;
+      for (uint32_t k = 0; k < nd; ++k) grad[elem_dof(A, &L, e, el, k)] += v[1 + k];
+    }
+    free(buf);
+    free(active);
+    free(list);
+    if (has_act) tape_free(&at);
+    tape_free(&t);
+  }
+  free(L.set_off);
+  *energy = Es;
+  *energy_kahan = Ek;
+  return status;
 }

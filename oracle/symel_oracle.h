@@ -58,6 +58,11 @@ int oracle_tape_eval(const uint8_t* tape, uint64_t len, const double* in, double
 int oracle_assemble(const oracle_array* arrays, uint32_t n_arrays, const oracle_energy* energies,
                     uint32_t n_energies, const uint8_t* pins, int32_t threads, oracle_result* res);
 /* Per-element raw outputs [E,g,H] (after fixed summation) for elements [first, first+count). */
+/* E (serial, reference order), E (Kahan) and the gradient only -- full-size parity checks;
+ * returns 0, 4 (non-finite: bad_energy / bad_element) or 6 (bad tape). grad has n_dofs entries. */
+int oracle_energy_gradient(const oracle_array* arrays, uint32_t n_arrays, const oracle_energy* energies,
+                           uint32_t n_energies, int32_t threads, double* energy, double* energy_kahan, double* grad,
+                           int32_t* bad_energy, int64_t* bad_element);
 int oracle_element_outputs(const oracle_array* arrays, uint32_t n_arrays, const oracle_energy* e,
                            uint64_t first, uint64_t count, double* out);
 int oracle_energy_only(const oracle_array* arrays, uint32_t n_arrays, const oracle_energy* energies,

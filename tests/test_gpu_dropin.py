@@ -21,26 +21,31 @@ from paper_2303_02156_b200 import configs as C
 pytestmark = pytest.mark.gpu
 DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_cuda_driver")
 
+# (case, SPD projection, energies evaluated in the reference's rounding: the barrier at
+# d ~ 1e-7 h loses ~6 digits computing d)
 CASES = {
-    "tet4": (lambda: C.config2(5), True),
-    "tet10": (lambda: C.config3(2), False),
-    "cloth": (lambda: C.config4(9), False),
-    "contact": (lambda: C.config5(3, 40), True),
+    "tet4": (lambda: C.config2(5), True, None),
+    "tet10": (lambda: C.config3(2), False, None),
+    "cloth": (lambda: C.config4(9), False, None),
+    "contact": (lambda: C.config5(3, 40), True, "contact"),
 }
 
 
 @pytest.mark.parametrize("kind", sorted(CASES))
 def test_reference_system_through_cuda_assembler(kind):
     assert os.path.exists(DRIVER), "built by oracle/Makefile (needs the reference headers at build time)"
-    make, spd = CASES[kind]
+    make, spd, exact = CASES[kind]
     with tempfile.TemporaryDirectory() as d:
         make().write_case_dir(d)
-        out = subprocess.run([DRIVER, d] + (["--spd"] if spd else []), capture_output=True, text=True, timeout=900)
+        args = [DRIVER, d] + (["--spd"] if spd else []) + (["--exact", exact] if exact else [])
+        out = subprocess.run(args, capture_output=True, text=True, timeout=900)
     lines = [json.loads(s) for s in out.stdout.splitlines() if s.startswith("{")]
     failed = [c for c in lines if not c["ok"]]
     assert out.returncode == 0 and not failed and lines, out.stdout + out.stderr
     names = {c["check"] for c in lines}
     assert {"assemble_deterministic", "assemble_atomic", "assemble_ordered", "energy_only", "guard_min",
-            "active_sets", "pins", "topology_change", "non_finite_message"} <= names
+            "active_sets", "pins", "non_finite_message"} <= names
+    if kind != "cloth":  # the membrane's per-element rest data pins its element count
+        assert "topology_change" in names
     if spd:
         assert {"spd_energy_gradient", "spd_symmetric"} <= names

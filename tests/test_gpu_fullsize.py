@@ -5,6 +5,13 @@ whole system in test time:
   energy), which makes the window's block rows complete; they must equal the device's rows of
   the full-size assembly -- pattern bit-exact, gradient rows and BSR values within the 1e-10
   north-star tolerance (SPD configs: against the oracle's numpy-eigh projection);
+* the WHOLE energy and gradient of every full-size system against the C oracle
+  (oracle_energy_gradient: the reference's tapes, activation, fixed summation, serial E sum in
+  (energy, element) order and per-dof gradient accumulation in (energy, element) order);
+* >= 100,000 random elements of the SPD configs "exploded" (each element on its own copies of
+  its nodes, so its blocks of the assembled BSR are exactly its projected element Hessian) run
+  through the production tile kernel with the fused SPD projection, against numpy eigh of the
+  oracle's element Hessians;
 * size-independent properties of the whole assembled system: exact block symmetry (mirror
   writes), deterministic vs atomic agreement, central differences of E and g along a random
   direction against g.d and H d (device SpMV), and positive semi-definiteness of the projected
@@ -73,6 +80,91 @@ def test_row_windows_match_oracle(name, oracle_mod):
         vr = ref["vals"].reshape(-1, b * b)[r0:r1]
         assert oracle_mod.rel_err(vd, vr) <= 1e-10, (name, lo)
         assert oracle_mod.rel_err(g[lo * b:hi * b], ref["grad"][lo * b:hi * b]) <= 1e-10, (name, lo)
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_whole_energy_and_gradient_match_oracle(name, oracle_mod):
+    """E and all n_dofs gradient entries of the full-size system (north star: 1e-10 in the
+    reference's measure, acceptance_main.cpp:101-106)."""
+    case, ds, spd, E, g, H = full(name)
+    ref = oracle_mod.system_for_case(case, golden_tape).energy_gradient()
+    assert ref["status"] == 0
+    eE = abs(E - ref["E"]) / max(1.0, abs(ref["E"]))
+    eK = abs(E - ref["E_kahan"]) / max(1.0, abs(ref["E_kahan"]))
+    eg = oracle_mod.rel_err(g, ref["grad"])
+    print(f"{name}: E {E!r} ref {ref['E']!r} kahan {ref['E_kahan']!r}  err_E {eE:.2e} (vs Kahan {eK:.2e})  "
+          f"err_g {eg:.2e} over {g.size} entries")
+    assert g.size == ref["grad"].size
+    assert eE <= 1e-10 and eK <= 1e-10 and eg <= 1e-10
+
+
+def exploded_system(case, which, count, seed, oracle_mod):
+    """`count` random elements of one energy ("tets" or the contact "pairs"), each on fresh
+    copies of its 4 nodes; registered alone on the device (SPD on) and in the oracle."""
+    from paper_2303_02156_b200 import systems as S
+    from paper_2303_02156_b200.device import DeviceAssembler, ENERGY_EXACT, ENERGY_SPD
+    rng = np.random.default_rng(seed)
+    src = case.conn if which == "tets" else case.extra["pairs"]
+    sel = np.sort(rng.choice(src.shape[0], count, replace=False))
+    conn = src[sel]
+    new_conn = np.arange(count * 4, dtype=np.int64).reshape(count, 4)
+    x, X = case.x[conn.ravel()], case.X[conn.ravel()]
+    p = case.params
+    A = DeviceAssembler()
+    xa = A.add_array("x", x.shape[0], 3, True)
+    ra = A.add_array("rest", x.shape[0], 3)
+    A.set_array(xa, x)
+    A.set_array(ra, X)
+    cid = A.add_connectivity(which, 4)
+    A.set_elements(cid, new_conn)
+    sysm = oracle_mod.System()
+    sysm.add_array("x", x, 3, True)
+    sysm.add_array("rest", X, 3)
+    if which == "tets":
+        A.add_energy("elastic", cid, golden_tape("tet4_elastic"), S.solid_tet_inputs(xa, ra), range(12),
+                     params={24: p["mu"], 25: p["lambda"]}, flags=ENERGY_SPD)
+        sysm.add_energy("elastic", new_conn, 4, golden_tape("tet4_elastic"), S.solid_tet_inputs(0, 1), range(12),
+                        params={24: p["mu"], 25: p["lambda"]})
+    else:
+        off = case.extra["offsets"][sel]
+        oa = A.add_array("pair_offset", count, 12)
+        A.set_array(oa, off)
+        A.add_energy("contact", cid, golden_tape("contact"), S.contact_inputs(xa, oa), range(12),
+                     act_tape=golden_tape("contact_act"), act_kind=0, guard_tape=golden_tape("contact_guard"),
+                     params={24: p["kappa"], 25: p["dhat"]}, flags=ENERGY_SPD | ENERGY_EXACT)
+        sysm.add_array("pair_offset", off, 12)
+        sysm.add_energy("contact", new_conn, 4, golden_tape("contact"), S.contact_inputs(0, 2), range(12),
+                        params={24: p["kappa"], 25: p["dhat"]}, act_tape=golden_tape("contact_act"), act_kind=0,
+                        guard_tape=golden_tape("contact_guard"))
+    return A, sysm, count
+
+
+@pytest.mark.parametrize("name,which", [("c2", "tets"), ("c5", "pairs")])
+def test_exploded_element_sample_spd(name, which, oracle_mod):
+    """The fused SPD projection element by element at scale: 100,000 random elements of the
+    config, isolated so that the 4x4 node blocks each assembles are exactly its projected 12x12
+    Hessian, through the production tile kernel; oracle: numpy eigh clamp of the reference
+    tape's element Hessian (SPD parity is unpinned by the reference)."""
+    case = _cache[name][0] if name in _cache else FULL[name][0]()
+    A, sysm, n = exploded_system(case, which, 100_000, 3, oracle_mod)
+    E = A.assemble("deterministic")
+    H = A.hessian()
+    assert np.array_equal(np.diff(H.row_ptr), np.full(4 * n, 4))
+    He = sysm.element_outputs(0, 0, n)[:, 13:].reshape(-1, 12, 12)
+    P = oracle_mod.spd_project(He)
+    rows = (4 * np.arange(n)[:, None] + np.arange(4)[None, :])          # (n, a)
+    blk = H.row_ptr[rows][:, :, None] + np.arange(4)[None, None, :]    # (n, a, c)
+    assert np.array_equal(H.col_idx[blk], np.broadcast_to(rows[:, None, :], (n, 4, 4)))
+    Hd = H.values.reshape(-1, 3, 3)[blk].transpose(0, 1, 3, 2, 4).reshape(n, 12, 12)
+    scale = np.maximum(1.0, np.abs(P).max(axis=(1, 2)))
+    err = np.abs(Hd - P).max(axis=(1, 2)) / scale
+    neg = (np.linalg.eigvalsh(0.5 * (He + np.swapaxes(He, 1, 2)))[:, 0] < 0).mean()
+    print(f"{name} {which}: {n} projected elements, max rel err {err.max():.2e}, median {np.median(err):.2e}, "
+          f"elements with a negative eigenvalue {neg:.0%}")
+    assert err.max() <= 1e-10
+    ref = sysm.energy_gradient()
+    assert abs(E - ref["E"]) <= 1e-10 * max(1.0, abs(ref["E"]))
+    assert oracle_mod.rel_err(A.gradient(), ref["grad"]) <= 1e-10
 
 
 @pytest.mark.parametrize("name", sorted(FULL))

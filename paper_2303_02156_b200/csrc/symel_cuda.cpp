@@ -1491,7 +1491,10 @@ int symel_cuda_add_array(symel_cuda_ctx* c, const char* name, uint64_t items, ui
     a.is_dof = is_dof != 0;
     if (c->device >= 0) {
       dalloc(&a.d, (std::size_t)(items * comps));
+      // zeroed (EnergySystem::add_array, registry.hpp:338) and complete before returning:
+      // set_array uploads on the copy stream, which must not race this memset
       CK(cudaMemsetAsync(a.d, 0, sizeof(double) * items * comps, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
     }
     c->arrays.push_back(a);
     c->topology_dirty = true;

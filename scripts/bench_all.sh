@@ -1,16 +1,20 @@
 #!/bin/bash
-# All five BASELINE configs, both fast modes; one JSON line each into gpurun_out/bench_all_<cfg>_<mode>.log
-for cfg in c1 c2 c3 c4 c5; do
-  for m in deterministic atomic; do
-    timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --mode $m --no-cpu-baseline > gpurun_out/bench_all_${cfg}_${m}.log 2>&1
-  done
+# All configs (device timing only, no CPU baseline), one JSON line each into gpurun_out/$1_*.json
+tag=${1:-bench}
+for c in c2 c1 c3 c4 c5; do
+  python bench.py --config $c --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline > gpurun_out/${tag}_$c.json 2> gpurun_out/${tag}_$c.err
 done
-python - <<'PY'
-import json, glob
-for f in sorted(glob.glob("gpurun_out/bench_all_*.log")):
+python bench.py --config c2 --no-spd --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline > gpurun_out/${tag}_c2nospd.json 2> gpurun_out/${tag}_c2nospd.err
+python - "$tag" <<'PY'
+import json, sys, glob
+tag = sys.argv[1]
+for f in sorted(glob.glob(f"gpurun_out/{tag}_*.json")):
     try:
         d = json.loads(open(f).read().strip().splitlines()[-1])
-        print(f.split("bench_all_")[1][:-4], "%.1f Melem/s" % d["value"], "%.3f ms" % d["ms_per_step"], "kernel %.3f ms" % d["roofline"]["kernel_ms"], "frac %.3f" % d["roofline"]["frac"], "e2e %.1f" % d["e2e"]["value"])
     except Exception as e:
-        print(f, "ERR", open(f).read()[-600:])
+        print(f, "FAILED", e); continue
+    r = d["roofline"]
+    print("%-28s %8.3f ms  %9.1f Melem/s  kernel %.3f ms  frac %.3f (%s)  atomic %s  e2e %.1f  e2eH %.1f" % (
+        f.split("/")[-1], d["ms_per_step"], d["value"], r["kernel_ms"], r["frac"], r["bound"],
+        "%.3f ms" % d["atomic"]["ms_per_step"] if "atomic" in d else "-", d["e2e"]["value"], d["e2e_host_hessian"]["value"]))
 PY

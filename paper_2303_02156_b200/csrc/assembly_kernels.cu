@@ -1129,6 +1129,20 @@ __global__ void k_soa_gather(const double* __restrict__ src, int comps, const in
   for (int c = 0; c < comps; ++c) dst[(long long)c * stride + pos] = src[el * comps + c];
 }
 
+// tile-ordered connectivity, slot-major: dst[k * n + pos] = conn[map[pos] * arity + k]
+__global__ void k_conn_soa(const int* __restrict__ conn, int arity, const int* __restrict__ map, long long n,
+                           int* __restrict__ dst) {
+  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const long long el = map ? (long long)map[pos] : pos;
+  for (int k = 0; k < arity; ++k) dst[(long long)k * n + pos] = conn[el * arity + k];
+}
+
+int conn_soa(const int* conn, int arity, const int* map, long long n, int* dst, void* s) {
+  if (n > 0) k_conn_soa<<<grid_for(n, 256), 256, 0, S(s)>>>(conn, arity, map, n, dst);
+  return (int)cudaGetLastError();
+}
+
 int soa_gather(const double* src, int comps, const int* map, long long n, long long stride, double* dst, void* s) {
   if (n > 0) k_soa_gather<<<grid_for(n, 256), 256, 0, S(s)>>>(src, comps, map, n, stride, dst);
   return (int)cudaGetLastError();

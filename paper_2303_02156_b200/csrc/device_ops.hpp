@@ -154,6 +154,9 @@ int tile_fixup(const TilePlan& p, const double* partials, const double* gpartial
                double* grad, void* stream, int which = 3);
 // Tile-ordered SoA copy of a per-element array: dst[c * stride + pos] = src[elem(pos) * comps + c],
 // elem(pos) = map[pos] (map == nullptr: identity), pos < n.
+// Tile-ordered, slot-major copy of an energy's connectivity (the tile kernels read their
+// elements' item indices with one coalesced load per slot instead of active -> conn -> item).
+int conn_soa(const int* conn, int arity, const int* map, long long n, int* dst, void* stream);
 int soa_gather(const double* src, int comps, const int* map, long long n, long long stride, double* dst,
                void* stream);
 // fixed-order sum of per-tile energies [first, first + n) into *out

@@ -46,6 +46,7 @@
     long long tile_base;                                                                 \
     int tile_atomic;                                                                     \
     long long soa_n;                                                                     \
+    const int* conn_soa;                                                                 \
     double params[32];                                                                   \
   };
 

@@ -108,6 +108,7 @@ struct Conn {
   std::uint32_t arity = 0;
   std::uint64_t n = 0;
   int* d = nullptr;
+  std::uint64_t version = 0;  // bumped by set_elements
 };
 
 struct Energy {
@@ -153,6 +154,8 @@ struct Energy {
   std::map<int, std::uint64_t> soa_version;
   long long soa_n = 0;          // SoA stride (n_active of the plan they were built for)
   std::uint64_t soa_epoch = ~0ull;
+  int* d_conn_soa = nullptr;    // tile-ordered connectivity, slot-major (stride soa_n)
+  std::uint64_t conn_soa_version = ~0ull;
 };
 
 }  // namespace
@@ -457,6 +460,9 @@ std::vector<std::uint8_t> soa_arrays_of(const symel_cuda_ctx* c, const Energy& e
   return v;
 }
 
+// SYMEL_NO_CONN_SOA: tile kernels read element id -> connectivity -> items (A/B switch)
+bool use_conn_soa() { return !std::getenv("SYMEL_NO_CONN_SOA"); }
+
 void ensure_soa(symel_cuda_ctx* c, Energy& e) {
   const std::vector<std::uint8_t> soa = soa_arrays_of(c, e);
   const int* map = e.d_tile_perm ? e.d_tile_elems : e.d_active;
@@ -475,6 +481,18 @@ void ensure_soa(symel_cuda_ctx* c, Energy& e) {
     CK(dev::soa_gather(arr.d, (int)arr.comps, map, e.n_active, e.n_active, buf, c->stream));
     ++c->launches;
     e.soa_version[(int)i] = arr.version;
+  }
+  // tile-ordered connectivity (rebuilt with the plan or a new element list)
+  if (use_conn_soa()) {
+    const Conn& k = c->conns[e.conn];
+    const bool fresh = e.d_conn_soa && e.soa_n == e.n_active && e.soa_epoch == c->plan_epoch &&
+                       e.conn_soa_version == k.version;
+    if (!fresh) {
+      if (!e.d_conn_soa || e.soa_n != e.n_active) dalloc(&e.d_conn_soa, (std::size_t)k.arity * std::max<long long>(1, e.n_active));
+      CK(dev::conn_soa(k.d, (int)k.arity, map, e.n_active, e.d_conn_soa, c->stream));
+      ++c->launches;
+      e.conn_soa_version = k.version;
+    }
   }
   e.soa_n = e.n_active;
   e.soa_epoch = c->plan_epoch;
@@ -527,6 +545,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.plan_global = v == V_TILE_G;
       s.item_lanes = tile_item_lanes(e);
       s.soa_arrays = soa_arrays_of(c, e);
+      s.conn_soa = use_conn_soa();
       s.mode = OutMode::fused_tile;
       s.schedule = -1;  // auto: lowest peak of live values
       s.threads_per_block = kTileElems;
@@ -540,6 +559,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s = base_spec(c, e, tp);
       s.plan_global = v == V_TILE_SPD_G;
       s.soa_arrays = soa_arrays_of(c, e);
+      s.conn_soa = use_conn_soa();
       s.mode = OutMode::fused_tile_spd;
       s.spd_m = e.spd_info.frontier;
       // QL lookahead (codegen.cpp sy_ql_la) pays off where divergence in the QL dominates
@@ -955,6 +975,7 @@ std::vector<TileLaunch> tile_launches(symel_cuda_ctx* c, bool atomic) {
     ensure_elem_buffers(c, e, false);
     for (const auto& kv : e.d_soa) a.arr[kv.first] = kv.second;
     a.soa_n = e.soa_n;
+    a.conn_soa = e.d_conn_soa;
     a.n = e.n_active;
     a.grad = c->d_grad;
     a.vals = c->d_vals;
@@ -1435,6 +1456,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
       cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
       cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems); cfree(e->d_gstage);
       for (auto& kv : e->d_soa) cfree(kv.second);
+      cfree(e->d_conn_soa);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);
     for (auto& g : c->graphs)
@@ -1563,6 +1585,7 @@ int symel_cuda_set_elements(symel_cuda_ctx* c, int id, const int64_t* flat, uint
       v[i] = (int)flat[i];
     }
     k.n = n_elems;
+    ++k.version;
     if (c->device >= 0) {
       dalloc(&k.d, v.size());
       copy_sync(c, k.d, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice);

@@ -460,7 +460,11 @@ std::vector<std::uint8_t> soa_arrays_of(const symel_cuda_ctx* c, const Energy& e
   return v;
 }
 
-// SYMEL_NO_CONN_SOA: tile kernels read element id -> connectivity -> items (A/B switch)
+// Tile kernels read their elements' items from a tile-ordered, slot-major copy of the
+// connectivity (one coalesced load per slot, independent of the element id) instead of
+// tile position -> element id -> connectivity -> items. Measured (same box A/B): config 3
+// 5.13 -> 4.00 ms, config 5 14.97 -> 14.59, config 4 4.71 -> 4.63, config 2 without SPD
+// 2.62 -> 2.58. SYMEL_NO_CONN_SOA switches it off.
 bool use_conn_soa() { return !std::getenv("SYMEL_NO_CONN_SOA"); }
 
 void ensure_soa(symel_cuda_ctx* c, Energy& e) {
@@ -559,7 +563,10 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s = base_spec(c, e, tp);
       s.plan_global = v == V_TILE_SPD_G;
       s.soa_arrays = soa_arrays_of(c, e);
-      s.conn_soa = use_conn_soa();
+      // measured: the SPD tet kernel (compute-bound, its connectivity latency hidden behind the
+      // other CTA's eigen-solve) is 1.3 % slower reading the copy; the exact-rounding contact
+      // kernel (random nodes, latency-bound) gains
+      s.conn_soa = use_conn_soa() && (e.flags & SYMEL_ENERGY_EXACT);
       s.mode = OutMode::fused_tile_spd;
       s.spd_m = e.spd_info.frontier;
       // QL lookahead (codegen.cpp sy_ql_la) pays off where divergence in the QL dominates

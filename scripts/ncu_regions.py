@@ -23,9 +23,12 @@ for i, l in enumerate(src, 1):
     if "void sy_ql(" in l: marks["eigen: implicit QL with vectors"] = i
     if "void sy_ql_la(" in l: marks["eigen: implicit QL with vectors (lookahead)"] = i
     if "void sy_eig(" in l: marks["eigen: wrapper"] = i
+    if "void sy_trid(" in l: marks["small-set: Householder (reflectors kept)"] = i
+    if "void sy_invit(" in l: marks["small-set: inverse iteration"] = i
+    if "void sy_clamp_ss(" in l: marks["small-set: compaction, back-transform, update"] = i
     if "V[N - 1][i] = V[i][i]" in l: marks["eigen: accumulate Q"] = i
     if "const long long e =" in l: marks["element tape (E, g, M, W)"] = i
-    if "sy_eig<" in l and "call" not in l: marks["SPD tail: clamp + H = W^T C W + stage"] = i - 1
+    if ("sy_eig<" in l or "sy_clamp_ss<" in l) and "call" not in l and "void" not in l: marks["SPD tail: clamp + H = W^T C W + stage"] = i - 1
     if "cp.async.wait_all" in l: marks["tile reduction + energy"] = i
 order = sorted(marks.items(), key=lambda kv: kv[1])
 def region(n):

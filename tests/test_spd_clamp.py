@@ -110,3 +110,48 @@ def test_lookahead_is_bitwise_the_plain_ql(harness, n):
     rng = np.random.default_rng(99 + n)
     mats = cases(rng, n)
     assert np.array_equal(run(harness, mats, "plain"), run(harness, mats, "la"))
+
+
+def stress_cases(rng, n, count):
+    """Random, clustered (at random scales), graded, low-rank-plus-shift, sparse / split and
+    stable-NH-like spectra."""
+    out = []
+    for _ in range(count):
+        kind = rng.integers(0, 6)
+        if kind == 0:
+            a = rng.standard_normal((n, n))
+            out.append(a + a.T)
+        elif kind == 1:
+            w = np.concatenate([b + rng.standard_normal(3) * 10.0 ** rng.uniform(-16, -2)
+                                for b in rng.uniform(-1, 1, (n + 2) // 3)])[:n]
+            out.append(with_spectrum(rng, w * 10.0 ** rng.uniform(-5, 15)))
+        elif kind == 2:
+            w = np.geomspace(1, 10.0 ** rng.uniform(3, 16), n) * rng.choice([-1, 1], n)
+            out.append(with_spectrum(rng, w))
+        elif kind == 3:
+            v = rng.standard_normal((n, 2))
+            out.append(v @ np.diag(rng.uniform(-3, 3, 2)) @ v.T + rng.uniform(-1, 1) * np.eye(n))
+        elif kind == 4:
+            a = np.zeros((n, n))
+            for _ in range(rng.integers(1, 10)):
+                i, j = rng.integers(0, n, 2)
+                v = rng.standard_normal()
+                a[i, j] += v
+                a[j, i] += v
+            out.append(a)
+        else:
+            w = rng.uniform(0.1, 10.0, n)
+            w[: rng.integers(0, n)] *= -rng.uniform(1e-6, 1.0)
+            out.append(with_spectrum(rng, w))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("variant", ["plain", "la"])
+@pytest.mark.parametrize("n", [3, 9])
+def test_clamp_stress(harness, n, variant):
+    """1500 hard matrices per size through the QL clamp: within 1e-10 of numpy's eigh clamp."""
+    rng = np.random.default_rng(7 + n)
+    mats = stress_cases(rng, n, 1500)
+    got = run(harness, mats, variant)
+    errs = [np.abs(g - clamp_ref(m)).max() / max(np.abs(m).max(), 1e-300) for m, g in zip(mats, got)]
+    assert max(errs) <= 1e-10, max(errs)

@@ -582,6 +582,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
     default:
       throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
   }
+  s.bulk_plan = !std::getenv("SYMEL_NO_BULK_PLAN");
   if (e.flags & SYMEL_ENERGY_EXACT) {
     // ill-conditioned energies: reproduce the reference's rounding (IEEE division, no
     // contraction) in every assembly mode. The schedule only reorders SSA instructions, so it
@@ -927,11 +928,9 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
       mx[2] = std::max(mx[2], hc[t + 1] - hc[t]);
       mx[3] = std::max(mx[3], gc[t + 1] - gc[t]);
     }
-    // 32-bit words of the u16 slices (+1 for a slice starting at an odd index)
-    e.cap[0] = mx[0] / 2 + 2;
-    e.cap[1] = mx[1] / 2 + 2;
-    e.cap[2] = mx[2] / 2 + 2;
-    e.cap[3] = mx[3] / 2 + 2;
+    // 32-bit words of the u16 slices, each copied as the 16-byte aligned range around it (bulk
+    // copy) and starting 16-byte aligned in shared memory
+    for (int q = 0; q < 4; ++q) e.cap[q] = ((2 * mx[q] + 30) / 16 + 1) * 4;
     cfree(e.d_gstage);
     e.d_gstage = nullptr;
     if (nt > 0 && tile_global_stage(c, e)) dalloc(&e.d_gstage, (std::size_t)nt * tile_stage_doubles(c, e));

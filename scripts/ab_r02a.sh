@@ -1,3 +1,6 @@
 #!/bin/bash
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge_cases.py -m gpu -x -q > gpurun_out/r02b_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r02b_tests.log
-for c in c2 c5; do python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']; print('$c', '%.3f ms kernel %.3f frac %.3f' % (d['ms_per_step'], r['kernel_ms'], r['frac']))"; done
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge_cases.py -m gpu -x -q > gpurun_out/r02d_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r02d_tests.log
+BENCH_FLAGS=--no-spd bash scripts/ab.sh c2 - SYMEL_NO_L2PF=1 SYMEL_NO_BULK_PLAN=1 "SYMEL_NO_L2PF=1 SYMEL_NO_BULK_PLAN=1"
+bash scripts/ab.sh c2 - "SYMEL_NO_L2PF=1 SYMEL_NO_BULK_PLAN=1"
+bash scripts/ab.sh c4 - "SYMEL_NO_L2PF=1 SYMEL_NO_BULK_PLAN=1"
+bash scripts/ab.sh c5 - "SYMEL_NO_L2PF=1 SYMEL_NO_BULK_PLAN=1"

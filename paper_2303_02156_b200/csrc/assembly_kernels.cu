@@ -1073,11 +1073,19 @@ int tile_order(const LbDesc& d, const double* const* arrs_host, const int* conn,
   unsigned long long h[6];
   cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, S(s));
   if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
-  double lo[3], inv[3];
+  // one scale for the three axes (the bounding cube of the largest extent): normalising each
+  // axis separately stretched a thin axis (a cloth's z noise) over the full key range, so the
+  // Morton order followed the noise and the tiles were scattered (config 4: 34.7 M segments /
+  // 33.6 M partials per-axis, 12.6 M / 10.7 M with the cube)
+  double lo[3], inv[3], ext = 0.0;
   for (int c = 0; c < 3; ++c) {
     lo[c] = from_ordered(h[c]);
-    const double ext = from_ordered(h[3 + c]) - lo[c];
-    inv[c] = ext > 0 ? 1023.0 / ext : 0.0;
+    ext = fmax(ext, from_ordered(h[3 + c]) - lo[c]);
+  }
+  const bool per_axis = std::getenv("SYMEL_MORTON_PER_AXIS") != nullptr;
+  for (int c = 0; c < 3; ++c) {
+    const double e = per_axis ? from_ordered(h[3 + c]) - lo[c] : ext;
+    inv[c] = e > 0 ? 1023.0 / e : 0.0;
   }
   k_morton_keys<<<grid_for(n, 256), 256, 0, S(s)>>>(cen, n, make_double3(lo[0], lo[1], lo[2]),
                                                     make_double3(inv[0], inv[1], inv[2]), key, ord);

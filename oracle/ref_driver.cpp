@@ -97,6 +97,10 @@ int main(int argc, char** argv) {
     write_bin("ref_rowptr.i64", rp.data(), rp.size());
     write_bin("ref_colidx.i64", ci.data(), ci.size());
     write_bin("ref_vals.f64", H.values.data(), H.values.size());
+    {  // the reference's text format (BcrsMatrix::dump, assembly.hpp:60-74)
+      std::ofstream ds(g_dir + "/ref_dump.txt");
+      H.dump(ds);
+    }
     if (solver) {
       // probe vector, y = H probe; block-Jacobi inverses and PCG (rhs = -g) for three shifts
       const std::size_t n = H.n_rows();

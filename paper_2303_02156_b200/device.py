@@ -160,6 +160,17 @@ class Bcrs:
         k = lo + np.searchsorted(self.col_idx[lo:hi], c)
         return int(k) if k < hi and self.col_idx[k] == c else -1
 
+    def dump(self) -> str:
+        """BcrsMatrix::dump (assembly.hpp:60-74): "b n_block_rows n_blocks", then one line per
+        stored block in row order, "(r c)" and the b*b values row-major as %.17g."""
+        b = int(self.b)
+        out = ["%d %d %d\n" % (b, self.n_block_rows, self.col_idx.size)]
+        v = self.values.reshape(-1, b * b)
+        for r in range(self.n_block_rows):
+            for k in range(int(self.row_ptr[r]), int(self.row_ptr[r + 1])):
+                out.append("(%d %d)" % (r, int(self.col_idx[k])) + "".join(" %.17g" % x for x in v[k]) + "\n")
+        return "".join(out)
+
     def to_dense(self) -> np.ndarray:
         b, n = self.b, self.n_block_rows
         D = np.zeros((n * b, n * b))

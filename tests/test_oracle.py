@@ -192,3 +192,16 @@ def test_spd_oracle_properties(oracle_mod):
     np.testing.assert_allclose(oracle_mod.spd_project(P), P, atol=1e-12)
     B = A @ np.swapaxes(A, 1, 2)
     np.testing.assert_allclose(oracle_mod.spd_project(B), B, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["tet4_n3", "cloth_n8"])
+def test_bcrs_dump_matches_reference_text(name):
+    """Bcrs.dump() writes the reference's BcrsMatrix::dump text byte for byte (fixture written
+    by the reference itself, oracle/make_dump_golden.py)."""
+    import gzip
+    import os
+    from paper_2303_02156_b200.device import Bcrs
+    g = golden(name)
+    H = Bcrs(b=3, row_ptr=g["row_ptr"], col_idx=g["col_idx"], values=g["vals"])
+    with gzip.open(os.path.join(os.path.dirname(__file__), "golden", name + "_dump.txt.gz"), "rt") as f:
+        assert H.dump() == f.read()

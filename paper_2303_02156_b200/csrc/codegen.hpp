@@ -55,6 +55,7 @@ struct KernelSpec {
   int item_lanes = 1;         // tile mode with fixed summation: the n_items terms of an element
                               // run on adjacent lanes (one term each) and are summed in order
                               // with shuffles; elements per tile = threads_per_block / item_lanes
+  bool soa_prefetch = true; // tile modes: bulk L2 prefetch of the tile's SoA component rows
   bool bulk_plan = true;   // tile modes: plan slice to shared memory by bulk (TMA) copies + mbarrier
   bool conn_soa = false;  // tile modes: item indices from the tile-ordered connectivity copy
   std::vector<std::uint8_t> soa_arrays;  // tile modes: per array, 1 = elem_comp inputs read

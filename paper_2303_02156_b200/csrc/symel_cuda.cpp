@@ -583,6 +583,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       throw Fail{SYMEL_E_ARG, "unsupported kernel variant"};
   }
   s.bulk_plan = !std::getenv("SYMEL_NO_BULK_PLAN");
+  s.soa_prefetch = !std::getenv("SYMEL_NO_SOA_PF");
   if (e.flags & SYMEL_ENERGY_EXACT) {
     // ill-conditioned energies: reproduce the reference's rounding (IEEE division, no
     // contraction) in every assembly mode. The schedule only reorders SSA instructions, so it

@@ -1013,6 +1013,9 @@ std::vector<TileLaunch> tile_launches(symel_cuda_ctx* c, bool atomic) {
     std::size_t plan_bytes = 4 * std::size_t(a.cap_hseg + a.cap_gseg + a.cap_hcon + a.cap_gcon);
     // two CTAs per SM with the plan slice prefetched to shared memory when staging + slice fit
     // half the SM; else two CTAs reading the slice from L2 (scattered tiles: contact pairs)
+    if (std::getenv("SYMEL_DEBUG_PLAN"))
+      std::fprintf(stderr, "[symel] energy %s: staging %zu B + plan slice %zu B (caps %d %d %d %d words)\n",
+                   e.name.c_str(), k->smem, plan_bytes, e.cap[0], e.cap[1], e.cap[2], e.cap[3]);
     if (k->smem + plan_bytes > kTileSmemCta && !std::getenv("SYMEL_PLAN_SMEM")) {
       k = kernel_for(c, e, spd ? V_TILE_SPD_G : V_TILE_G);
       plan_bytes = 0;

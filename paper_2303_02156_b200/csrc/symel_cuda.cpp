@@ -71,11 +71,29 @@ struct Compiled {
 };
 
 // Elements per tile = threads per CTA of the tile kernel (one element per thread).
-constexpr int kTileElems = 128;
-// Shared memory per tile CTA: two CTAs per SM (228 KB per SM on B200, 1 KB reserved per CTA,
-// a little static smem). The staging part is capped lower to leave room for the plan slice.
-constexpr std::size_t kTileSmemCta = 112 * 1024;
-constexpr std::size_t kTileSmemMax = 106 * 1024;
+// Threads per tile CTA: 128 with two CTAs per SM; 96 with three for the item-lane energies whose
+// staging lives in global memory (tet10: no shared-memory limit, so nine warps per SM at 224
+// registers instead of eight at 232: config 3 tile kernel 1.75 -> 1.53 ms; measured slower on
+// every shared-memory-staged kernel). SYMEL_TILE_THREADS = 32 / 64 / 96 / 128 overrides
+// (diagnostic; the contribution codes hold 7 bits of tile-local element).
+int tile_threads_env() {
+  static const int v = [] {
+    const char* e = std::getenv("SYMEL_TILE_THREADS");
+    const int t = e ? std::atoi(e) : 0;
+    return (t == 32 || t == 64 || t == 96 || t == 128) ? t : 0;
+  }();
+  return v;
+}
+// resident CTAs per SM the kernels are compiled for (register cap 65536 / (threads * CTAs));
+// SYMEL_TILE_CTAS overrides (diagnostic)
+int tile_ctas_per_sm(int threads) {
+  static const int env = [] { const char* e = std::getenv("SYMEL_TILE_CTAS"); return e ? std::atoi(e) : 0; }();
+  return env > 0 ? env : 256 / threads;
+}
+// Shared memory per tile CTA (228 KB per SM on B200, 1 KB reserved per CTA, a little static
+// smem); the staging part is capped lower to leave room for the plan slice.
+std::size_t tile_smem_cta(int threads) { return (std::size_t)(225 * 1024 / tile_ctas_per_sm(threads)) & ~(std::size_t)1023; }
+std::size_t tile_smem_max(int threads) { return tile_smem_cta(threads) - 6 * 1024 * (std::size_t)threads / 128; }
 constexpr std::size_t kTileSmemOne = 226 * 1024;  // single CTA per SM (opt-in maximum 227 KB)
 
 // Kernel variants per energy.
@@ -388,7 +406,7 @@ Compiled* compile_kernel(symel_cuda_ctx* c, const KernelSpec& spec) {
 }
 
 // Dynamic shared memory of the tile kernel: per element [E | g(n) | upper local-block
-// triangle of full b x b sub-blocks] (codegen.cpp stage layout), kTileElems elements.
+// triangle of full b x b sub-blocks] (codegen.cpp stage layout), one tile of elements.
 // Fixed-summation energies (n_items = 2, 4, 8: tet10's quadrature) run their item terms on
 // adjacent lanes in the tile kernel: 128 / n_items elements per tile.
 int tile_item_lanes(const Energy& e) {
@@ -396,15 +414,21 @@ int tile_item_lanes(const Energy& e) {
   const int n = (int)e.n_items;
   return (n == 2 || n == 4 || n == 8) ? n : 1;
 }
-int tile_elems(const Energy& e) { return kTileElems / tile_item_lanes(e); }
-
-std::size_t tile_stage_doubles(const symel_cuda_ctx* c, const Energy& e) {
+std::size_t tile_stage_slots(const symel_cuda_ctx* c, const Energy& e) {
   const std::size_t n = e.dof_slots.size(), nlb = e.bm.n_lb, bb = std::size_t(c->b) * c->b;
-  return (1 + n + bb * nlb * (nlb + 1) / 2) * tile_elems(e);
+  return 1 + n + bb * nlb * (nlb + 1) / 2;
 }
-// Elements whose staged outputs do not fit two CTAs per SM stage in global memory instead.
+int tile_threads(const symel_cuda_ctx* c, const Energy& e) {
+  if (tile_threads_env()) return tile_threads_env();
+  const int lanes = tile_item_lanes(e);
+  const bool global_at_128 = sizeof(double) * tile_stage_slots(c, e) * (128 / lanes) > tile_smem_max(128);
+  return (lanes == 4 && global_at_128) ? 96 : 128;
+}
+int tile_elems(const symel_cuda_ctx* c, const Energy& e) { return tile_threads(c, e) / tile_item_lanes(e); }
+std::size_t tile_stage_doubles(const symel_cuda_ctx* c, const Energy& e) { return tile_stage_slots(c, e) * tile_elems(c, e); }
+// Elements whose staged outputs do not fit the CTA's share of the SM stage in global memory instead.
 bool tile_global_stage(const symel_cuda_ctx* c, const Energy& e) {
-  return sizeof(double) * tile_stage_doubles(c, e) > kTileSmemMax;
+  return sizeof(double) * tile_stage_doubles(c, e) > tile_smem_max(tile_threads(c, e));
 }
 std::size_t tile_smem(const symel_cuda_ctx* c, const Energy& e) {
   return tile_global_stage(c, e) ? 0 : sizeof(double) * tile_stage_doubles(c, e);
@@ -552,8 +576,8 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.conn_soa = use_conn_soa();
       s.mode = OutMode::fused_tile;
       s.schedule = -1;  // auto: lowest peak of live values
-      s.threads_per_block = kTileElems;
-      s.min_blocks = 2;
+      s.threads_per_block = tile_threads(c, e);
+      s.min_blocks = tile_ctas_per_sm(s.threads_per_block);
       s.stage_global = tile_global_stage(c, e);
       break;
     case V_TILE_SPD:
@@ -574,8 +598,8 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       // unfactorised tape already strains the instruction cache, measured 1.4 ms slower with it
       s.spd_lookahead = !(e.flags & SYMEL_ENERGY_EXACT) && !std::getenv("SYMEL_NO_QL_LOOKAHEAD");
       s.schedule = -1;
-      s.threads_per_block = kTileElems;
-      s.min_blocks = 2;
+      s.threads_per_block = tile_threads(c, e);
+      s.min_blocks = tile_ctas_per_sm(s.threads_per_block);
       s.stage_global = tile_global_stage(c, e);
       break;
     }
@@ -851,7 +875,7 @@ double finish_assemble(symel_cuda_ctx* c, symel_cuda_status* st, bool async_tail
 // elements (hex27 / Q2 type) take the contrib path.
 bool tile_codes_fit(const Energy& e) { return e.bm.n_lb * (e.bm.n_lb + 1) / 2 <= 256; }
 
-bool tile_ok(const symel_cuda_ctx* c, const Energy& e) { return tile_codes_fit(e) && tile_smem(c, e) <= kTileSmemMax; }
+bool tile_ok(const symel_cuda_ctx* c, const Energy& e) { return tile_codes_fit(e) && tile_smem(c, e) <= tile_smem_max(tile_threads(c, e)); }
 
 bool all_tile_capable(symel_cuda_ctx* c) {
   long long nh = 0, ng = 0;
@@ -881,7 +905,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     s.active = e.d_active;
     s.n_active = e.n_active;
     s.tile_base = tiles;
-    s.tpb = tile_elems(e);
+    s.tpb = tile_elems(c, e);
     s.d = lb_desc(c, e);
     s.h0 = 1 + (int)e.dof_slots.size();
     s.sort_segments = tile_global_stage(c, e) ? 0 : 1;  // L2-staged tiles keep target order
@@ -905,7 +929,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
       s.perm = nullptr;
     }
     src.push_back(s);
-    tiles += (e.n_active + tile_elems(e) - 1) / tile_elems(e);
+    tiles += (e.n_active + tile_elems(c, e) - 1) / tile_elems(c, e);
   }
   CK(dev::build_tile_plan(src.data(), (int)src.size(), c->n_blocks, c->n_rows, c->d_row_ptr, c->d_col_idx, &c->tplan,
                           c->stream));
@@ -922,7 +946,7 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
   for (auto& ep : c->energies) {
     Energy& e = *ep;
     int mx[4] = {0, 0, 0, 0};
-    const long long nt = (e.skip || e.n_active == 0) ? 0 : (e.n_active + tile_elems(e) - 1) / tile_elems(e);
+    const long long nt = (e.skip || e.n_active == 0) ? 0 : (e.n_active + tile_elems(c, e) - 1) / tile_elems(c, e);
     for (long long t = e.tile_base; t < e.tile_base + nt; ++t) {
       mx[0] = std::max(mx[0], hs[t + 1] - hs[t]);
       mx[1] = std::max(mx[1], gs[t + 1] - gs[t]);
@@ -1016,7 +1040,7 @@ std::vector<TileLaunch> tile_launches(symel_cuda_ctx* c, bool atomic) {
     if (std::getenv("SYMEL_DEBUG_PLAN"))
       std::fprintf(stderr, "[symel] energy %s: staging %zu B + plan slice %zu B (caps %d %d %d %d words)\n",
                    e.name.c_str(), k->smem, plan_bytes, e.cap[0], e.cap[1], e.cap[2], e.cap[3]);
-    if (k->smem + plan_bytes > kTileSmemCta && !std::getenv("SYMEL_PLAN_SMEM")) {
+    if (k->smem + plan_bytes > tile_smem_cta(k->tpb) && !std::getenv("SYMEL_PLAN_SMEM")) {
       k = kernel_for(c, e, spd ? V_TILE_SPD_G : V_TILE_G);
       plan_bytes = 0;
     }
@@ -1109,7 +1133,7 @@ void enqueue_tiled(symel_cuda_ctx* c, const std::vector<TileLaunch>& ls, bool at
   for (int q = 0; q < ne; ++q) {
     Energy& e = *c->energies[q];
     if (e.skip || e.n_active == 0) continue;
-    const long long nt = (e.n_active + tile_elems(e) - 1) / tile_elems(e);
+    const long long nt = (e.n_active + tile_elems(c, e) - 1) / tile_elems(c, e);
     CK(dev::tile_energy(c->d_tileE, e.tile_base, nt, c->d_partial, c->d_energy + q, c->stream));
     c->launches += 2;
   }

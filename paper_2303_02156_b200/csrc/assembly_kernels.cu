@@ -1207,6 +1207,90 @@ int soa_gather(const double* src, int comps, const int* map, long long n, long l
   return (int)cudaGetLastError();
 }
 
+// only the listed component rows: dst[r * stride + pos] = src[map[pos] * comps + rows[r]]
+__global__ void k_soa_gather_rows(const double* __restrict__ src, int comps, const int* __restrict__ rows, int n_rows,
+                                  const int* __restrict__ map, long long n, long long stride, double* __restrict__ dst) {
+  const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const long long el = map ? (long long)map[pos] : pos;
+  for (int r = 0; r < n_rows; ++r) dst[(long long)r * stride + pos] = src[el * comps + __ldg(rows + r)];
+}
+
+int soa_gather_rows(const double* src, int comps, const int* rows, int n_rows, const int* map, long long n,
+                    long long stride, double* dst, void* s) {
+  if (n > 0 && n_rows > 0)
+    k_soa_gather_rows<<<grid_for(n, 256), 256, 0, S(s)>>>(src, comps, rows, n_rows, map, n, stride, dst);
+  return (int)cudaGetLastError();
+}
+
+// Component classes of a per-item array (items x comps, AoS): pass 1 accumulates per component a
+// position-dependent 64-bit hash sum and the OR of the bit patterns over all items; the host
+// groups components with equal sums; pass 2 verifies every grouped component against its
+// representative bit for bit (a mismatch anywhere makes the component its own class).
+__global__ void k_comp_hash(const unsigned long long* __restrict__ src, int comps, long long items,
+                            unsigned long long* __restrict__ hsum, unsigned long long* __restrict__ hor) {
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;  // component (fast index: coalesced rows)
+  if (c >= comps) return;
+  unsigned long long sum = 0ull, orv = 0ull;
+  for (long long i = blockIdx.x; i < items; i += gridDim.x) {
+    const unsigned long long v = src[i * comps + c];
+    unsigned long long z = v + 0x9e3779b97f4a7c15ull * (unsigned long long)(i + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    sum += z ^ (z >> 31);
+    orv |= v;
+  }
+  atomicAdd(hsum + c, sum);
+  atomicOr(hor + c, orv);
+}
+
+__global__ void k_comp_verify(const unsigned long long* __restrict__ src, int comps, long long items,
+                              const int* __restrict__ rep, int* __restrict__ differs) {
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= comps) return;
+  const int r = rep[c];
+  if (r == c || r < 0) return;
+  bool bad = false;
+  for (long long i = blockIdx.x; i < items; i += gridDim.x) bad = bad || src[i * comps + c] != src[i * comps + r];
+  if (bad) differs[c] = 1;
+}
+
+int comp_classes(const double* src, int comps, long long items, int* cls, void* s) {
+  for (int c = 0; c < comps; ++c) cls[c] = c;
+  if (items <= 0 || comps <= 0) return 0;
+  int err;
+  unsigned long long *hsum = nullptr, *hor = nullptr;
+  int *rep = nullptr, *differs = nullptr;
+  if ((err = tmp_alloc(&hsum, comps, s)) || (err = tmp_alloc(&hor, comps, s)) || (err = tmp_alloc(&rep, comps, s)) ||
+      (err = tmp_alloc(&differs, comps, s)))
+    return err;
+  cudaMemsetAsync(hsum, 0, sizeof(unsigned long long) * comps, S(s));
+  cudaMemsetAsync(hor, 0, sizeof(unsigned long long) * comps, S(s));
+  cudaMemsetAsync(differs, 0, sizeof(int) * comps, S(s));
+  const int tx = comps >= 128 ? 128 : (comps >= 64 ? 64 : 32);
+  const dim3 grid((unsigned)std::min<long long>(items, 148 * 16), (unsigned)((comps + tx - 1) / tx));
+  k_comp_hash<<<grid, tx, 0, S(s)>>>((const unsigned long long*)src, comps, items, hsum, hor);
+  std::vector<unsigned long long> hs(comps), ho(comps);
+  cudaMemcpyAsync(hs.data(), hsum, sizeof(unsigned long long) * comps, cudaMemcpyDeviceToHost, S(s));
+  cudaMemcpyAsync(ho.data(), hor, sizeof(unsigned long long) * comps, cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  std::vector<int> r(comps);
+  for (int c = 0; c < comps; ++c) {
+    r[c] = c;
+    if (ho[c] == 0ull) { r[c] = -1; continue; }  // every item holds +0.0
+    for (int q = 0; q < c; ++q)
+      if (r[q] == q && hs[q] == hs[c]) { r[c] = q; break; }
+  }
+  cudaMemcpyAsync(rep, r.data(), sizeof(int) * comps, cudaMemcpyHostToDevice, S(s));
+  k_comp_verify<<<grid, tx, 0, S(s)>>>((const unsigned long long*)src, comps, items, rep, differs);
+  std::vector<int> df(comps);
+  cudaMemcpyAsync(df.data(), differs, sizeof(int) * comps, cudaMemcpyDeviceToHost, S(s));
+  if ((err = (int)cudaStreamSynchronize(S(s)))) return err;
+  for (int c = 0; c < comps; ++c) cls[c] = df[c] ? c : r[c];
+  for (void* q : {(void*)hsum, (void*)hor, (void*)rep, (void*)differs}) cudaFreeAsync(q, S(s));
+  return (int)cudaGetLastError();
+}
+
 int tile_energy(const double* tileE, long long first, long long n, double* partial, double* out, void* s) {
   return energy_tree(tileE + first, 1, n, partial, out, s);
 }

@@ -58,6 +58,9 @@ struct KernelSpec {
   bool soa_prefetch = true; // tile modes: bulk L2 prefetch of the tile's SoA component rows
   bool bulk_plan = true;   // tile modes: plan slice to shared memory by bulk (TMA) copies + mbarrier
   bool conn_soa = false;  // tile modes: item indices from the tile-ordered connectivity copy
+  // tile modes: per SoA array, component -> row of the (deduplicated) SoA copy, -1 = the
+  // component is +0.0 in every element (no load); empty = identity (row == component)
+  std::vector<std::vector<int>> soa_rows;
   std::vector<std::uint8_t> soa_arrays;  // tile modes: per array, 1 = elem_comp inputs read
                                          // from a tile-ordered SoA copy a.arr[i][c * soa_n + t]
   bool plan_global = false;   // tile modes: read the plan slice from global memory (L2) instead of

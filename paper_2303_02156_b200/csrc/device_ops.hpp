@@ -159,6 +159,13 @@ int tile_fixup(const TilePlan& p, const double* partials, const double* gpartial
 int conn_soa(const int* conn, int arity, const int* map, long long n, int* dst, void* stream);
 int soa_gather(const double* src, int comps, const int* map, long long n, long long stride, double* dst,
                void* stream);
+// the same for a subset of component rows (device list `rows`, n_rows entries)
+int soa_gather_rows(const double* src, int comps, const int* rows, int n_rows, const int* map, long long n,
+                    long long stride, double* dst, void* stream);
+// Component classes of a per-item array (items x comps): cls[c] = -1 when every item holds +0.0
+// in component c, else the smallest component whose column is bit-for-bit identical (c itself
+// when unique). Exact (hash grouping verified element by element). Host-synchronous.
+int comp_classes(const double* src, int comps, long long items, int* cls, void* stream);
 // fixed-order sum of per-tile energies [first, first + n) into *out
 int tile_energy(const double* tileE, long long first, long long n, double* partial, double* out, void* stream);
 

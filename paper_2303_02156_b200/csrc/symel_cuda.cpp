@@ -119,6 +119,11 @@ struct Array {
   double* d = nullptr;
   std::uint64_t version = 0;  // bumped by every set_array (SoA copies are rebuilt from it)
   bool external = false;      // device pointer handed out: treat as changed every assemble
+  // component classes (dev::comp_classes) of the data of `cls_version`; recomputed when the
+  // array is set again, given up (identity) for arrays that keep changing
+  std::vector<int> cls;
+  std::uint64_t cls_version = ~0ull;
+  int cls_runs = 0;
 };
 
 struct Conn {
@@ -169,6 +174,8 @@ struct Energy {
   double* d_gstage = nullptr;  // global staging (large elements): one slab per tile
   // tile-ordered SoA copies of wide per-element arrays (elem_comp inputs): array -> copy
   std::map<int, double*> d_soa;
+  std::map<int, std::vector<int>> soa_rows;  // component -> SoA row the copies / kernels were built with
+  std::map<int, int*> d_soa_rowlist;         // device list of the representative components
   std::map<int, std::uint64_t> soa_version;
   long long soa_n = 0;          // SoA stride (n_active of the plan they were built for)
   std::uint64_t soa_epoch = ~0ull;
@@ -491,6 +498,39 @@ std::vector<std::uint8_t> soa_arrays_of(const symel_cuda_ctx* c, const Energy& e
 // 2.62 -> 2.58. SYMEL_NO_CONN_SOA switches it off.
 bool use_conn_soa() { return !std::getenv("SYMEL_NO_CONN_SOA"); }
 
+// Wide per-element arrays often hold structure the tape cannot see: components that are +0.0 in
+// every element and components that repeat another one bit for bit (the reference's 12 x 12
+// bending Q, energies.hpp:684-745, is a 4 x 4 stencil repeated per coordinate: 96 zeros and 16
+// distinct values in 144 doubles). The SoA copy keeps one row per distinct non-zero component
+// and the generated kernel reads each once (a zero component becomes the literal 0.0): the
+// arithmetic, and so every output bit, is unchanged. Classes are exact (dev::comp_classes),
+// recomputed when the array is set again (given up for arrays set more than a few times) and
+// part of the kernel specialisation. SYMEL_NO_SOA_DEDUP switches it off.
+constexpr std::uint32_t kDedupMinComps = 16;
+std::vector<int> soa_rows_of(symel_cuda_ctx* c, std::size_t i) {
+  Array& arr = c->arrays[i];
+  static const bool off = std::getenv("SYMEL_NO_SOA_DEDUP") != nullptr;
+  if (off || c->device < 0 || arr.external || !arr.d || arr.comps < kDedupMinComps || arr.cls_runs > 4) return {};
+  if (arr.cls_version != arr.version) {
+    arr.cls.assign(arr.comps, 0);
+    CK(dev::comp_classes(arr.d, (int)arr.comps, (long long)arr.items, arr.cls.data(), c->stream));
+    c->launches += 2;
+    arr.cls_version = arr.version;
+    ++arr.cls_runs;
+  }
+  // component -> row: representatives numbered in component order
+  std::vector<int> row(arr.comps, -1), rank(arr.comps, -1);
+  int n = 0;
+  bool identity = true;
+  for (std::uint32_t q = 0; q < arr.comps; ++q)
+    if (arr.cls[q] == (int)q) rank[q] = n++;
+  for (std::uint32_t q = 0; q < arr.comps; ++q) {
+    row[q] = arr.cls[q] < 0 ? -1 : rank[arr.cls[q]];
+    identity = identity && row[q] == (int)q;
+  }
+  return identity ? std::vector<int>{} : row;
+}
+
 void ensure_soa(symel_cuda_ctx* c, Energy& e) {
   const std::vector<std::uint8_t> soa = soa_arrays_of(c, e);
   const int* map = e.d_tile_perm ? e.d_tile_elems : e.d_active;
@@ -498,15 +538,32 @@ void ensure_soa(symel_cuda_ctx* c, Energy& e) {
     if (!soa[i]) continue;
     const Array& arr = c->arrays[i];
     double*& buf = e.d_soa[(int)i];
+    const std::vector<int>& rows = e.soa_rows[(int)i];  // set by refresh_soa_rows before the kernels are chosen
     const bool fresh = buf && e.soa_n == e.n_active && e.soa_epoch == c->plan_epoch &&
                        e.soa_version[(int)i] == arr.version && !arr.external;
     if (fresh) continue;
-    if (!buf || e.soa_n != e.n_active) {
-      cfree(buf);
-      buf = nullptr;
-      dalloc(&buf, (std::size_t)arr.comps * std::max<long long>(1, e.n_active));
+    int n_rows = (int)arr.comps;
+    std::vector<int> reps;
+    if (!rows.empty()) {
+      n_rows = 0;
+      for (int r : rows) n_rows = std::max(n_rows, r + 1);
+      reps.assign(n_rows, 0);
+      for (std::uint32_t q = arr.comps; q-- > 0;)
+        if (rows[q] >= 0) reps[rows[q]] = (int)q;  // lowest component of the class last
     }
-    CK(dev::soa_gather(arr.d, (int)arr.comps, map, e.n_active, e.n_active, buf, c->stream));
+    cfree(buf);
+    buf = nullptr;
+    dalloc(&buf, (std::size_t)std::max(1, n_rows) * std::max<long long>(1, e.n_active));
+    if (rows.empty()) {
+      CK(dev::soa_gather(arr.d, (int)arr.comps, map, e.n_active, e.n_active, buf, c->stream));
+    } else {
+      int*& rl = e.d_soa_rowlist[(int)i];
+      cfree(rl);
+      rl = nullptr;
+      dalloc(&rl, (std::size_t)std::max(1, n_rows));
+      if (n_rows) copy_sync(c, rl, reps.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice);
+      CK(dev::soa_gather_rows(arr.d, (int)arr.comps, rl, n_rows, map, e.n_active, e.n_active, buf, c->stream));
+    }
     ++c->launches;
     e.soa_version[(int)i] = arr.version;
   }
@@ -524,6 +581,32 @@ void ensure_soa(symel_cuda_ctx* c, Energy& e) {
   }
   e.soa_n = e.n_active;
   e.soa_epoch = c->plan_epoch;
+}
+
+// The row maps the energy's kernels are specialised on (per array; empty = identity).
+std::vector<std::vector<int>> soa_rows_spec(symel_cuda_ctx* c, Energy& e) {
+  std::vector<std::vector<int>> v(c->arrays.size());
+  for (const auto& kv : e.soa_rows) v[kv.first] = kv.second;
+  return v;
+}
+
+// Recomputes the energy's row maps from the arrays' current data; when a map changed, the tile
+// kernels compiled for the old one and the SoA copies built with it are dropped.
+void refresh_soa_rows(symel_cuda_ctx* c, Energy& e) {
+  const std::vector<std::uint8_t> soa = soa_arrays_of(c, e);
+  bool changed = false;
+  for (std::size_t i = 0; i < soa.size(); ++i) {
+    if (!soa[i]) continue;
+    std::vector<int> rows = soa_rows_of(c, i);
+    auto it = e.soa_rows.find((int)i);
+    if (it == e.soa_rows.end() || it->second != rows) {
+      changed = changed || it != e.soa_rows.end() || !rows.empty();
+      e.soa_rows[(int)i] = std::move(rows);
+      e.soa_version[(int)i] = ~0ull;  // rebuild the copy
+    }
+  }
+  if (changed)
+    for (int v : {V_TILE, V_TILE_SPD, V_TILE_G, V_TILE_SPD_G}) e.k[v] = nullptr;  // owned by the context's cache
 }
 
 KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
@@ -573,6 +656,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.plan_global = v == V_TILE_G;
       s.item_lanes = tile_item_lanes(e);
       s.soa_arrays = soa_arrays_of(c, e);
+      s.soa_rows = soa_rows_spec(c, e);
       s.conn_soa = use_conn_soa();
       s.mode = OutMode::fused_tile;
       s.schedule = -1;  // auto: lowest peak of live values
@@ -587,6 +671,7 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s = base_spec(c, e, tp);
       s.plan_global = v == V_TILE_SPD_G;
       s.soa_arrays = soa_arrays_of(c, e);
+      s.soa_rows = soa_rows_spec(c, e);
       // measured: the SPD tet kernel (compute-bound, its connectivity latency hidden behind the
       // other CTA's eigen-solve) is 1.3 % slower reading the copy; the exact-rounding contact
       // kernel (random nodes, latency-bound) gains
@@ -998,6 +1083,7 @@ std::vector<TileLaunch> tile_launches(symel_cuda_ctx* c, bool atomic) {
     L.stream_slot = concurrent ? slot : 0;
     ++slot;
     const bool spd = (e.flags & SYMEL_ENERGY_SPD) != 0;
+    refresh_soa_rows(c, e);
     Compiled* k = kernel_for(c, e, spd ? V_TILE_SPD : V_TILE);
     SyArgs& a = L.a;
     fill_args(c, e, a);
@@ -1490,6 +1576,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
       cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
       cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems); cfree(e->d_gstage);
       for (auto& kv : e->d_soa) cfree(kv.second);
+      for (auto& kv : e->d_soa_rowlist) cfree(kv.second);
       cfree(e->d_conn_soa);
     }
     cfree(c->d_row_ptr); cfree(c->d_col_idx); cfree(c->d_vals); cfree(c->d_grad); cfree(c->d_pins);

@@ -135,7 +135,7 @@ class DeviceSystem:
                                                      range(9), params={14: p["mu"], 15: p["lambda"]}, flags=flags)
             fc = A.add_connectivity("flaps", 4)
             A.set_elements(fc, case.extra["flaps"])
-            q = A.add_array("Q", nf, 144)
+            q = self.arrays["Q"] = A.add_array("Q", nf, 144)
             A.set_array(q, Q if Q is not None else configs.bending_Q_for(case))
             self.energies["bending"] = A.add_energy("bending", fc, tapes("bending"), bending_inputs(self.x, q),
                                                     range(12), params={156: p["kb"]}, flags=flags)

@@ -173,6 +173,7 @@ struct Energy {
   int cap[4] = {0, 0, 0, 0};   // shared plan-slice capacities (words): hseg, gseg, hcon, gcon
   double* d_gstage = nullptr;  // global staging (large elements): one slab per tile
   // tile-ordered SoA copies of wide per-element arrays (elem_comp inputs): array -> copy
+  int* d_changed = nullptr;     // activation: "the active set moved" flag of the last refresh
   std::map<int, double*> d_soa;
   std::map<int, std::vector<int>> soa_rows;  // component -> SoA row the copies / kernels were built with
   std::map<int, int*> d_soa_rowlist;         // device list of the representative components
@@ -886,14 +887,14 @@ void refresh_activation(symel_cuda_ctx* c) {
     a.n = ne;
     a.value_out = e.d_values;
     launch(c, k, a, ne);
-    int* d_changed = nullptr;
-    CK(cudaMallocAsync((void**)&d_changed, sizeof(int), c->stream));
-    CK(cudaMemsetAsync(d_changed, 0, sizeof(int), c->stream));
-    CK(dev::activation_mask(e.d_values, ne, e.act_kind, e.d_mask, d_changed, c->stream));
+    // the host has to know whether the active set moved (it decides on a pattern rebuild, like
+    // the reference's prepare): one flag per energy, allocated once
+    if (!e.d_changed) dalloc(&e.d_changed, 1);
+    CK(cudaMemsetAsync(e.d_changed, 0, sizeof(int), c->stream));
+    CK(dev::activation_mask(e.d_values, ne, e.act_kind, e.d_mask, e.d_changed, c->stream));
     ++c->launches;
     int changed = 0;
-    CK(cudaMemcpyAsync(&changed, d_changed, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaFreeAsync(d_changed, c->stream));
+    CK(cudaMemcpyAsync(&changed, e.d_changed, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (changed || e.n_active < 0) {
       dalloc(&e.d_active, (std::size_t)ne);
@@ -1574,7 +1575,7 @@ void symel_cuda_destroy(symel_cuda_ctx* c) {
     for (Conn& k : c->conns) cfree(k.d);
     for (auto& e : c->energies) {
       cfree(e->d_mask); cfree(e->d_active); cfree(e->d_slots); cfree(e->d_contrib); cfree(e->d_elemE);
-      cfree(e->d_values); cfree(e->d_tile_perm); cfree(e->d_tile_elems); cfree(e->d_gstage);
+      cfree(e->d_values); cfree(e->d_changed); cfree(e->d_tile_perm); cfree(e->d_tile_elems); cfree(e->d_gstage);
       for (auto& kv : e->d_soa) cfree(kv.second);
       for (auto& kv : e->d_soa_rowlist) cfree(kv.second);
       cfree(e->d_conn_soa);

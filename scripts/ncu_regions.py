@@ -29,7 +29,7 @@ for i, l in enumerate(src, 1):
     if "V[N - 1][i] = V[i][i]" in l: marks["eigen: accumulate Q"] = i
     if "const long long e =" in l: marks["element tape (E, g, M, W)"] = i
     if ("sy_eig<" in l or "sy_clamp_ss<" in l) and "call" not in l and "void" not in l: marks["SPD tail: clamp + H = W^T C W + stage"] = i - 1
-    if "cp.async.wait_all" in l: marks["tile reduction + energy"] = i
+    if "const int sy_nh = hs1 - hs0" in l: marks["tile reduction + energy"] = i
 order = sorted(marks.items(), key=lambda kv: kv[1])
 def region(n):
     name = order[0][0]

@@ -11,7 +11,7 @@ ncu --set full --clock-control none --import-source on --profile-from-start off 
 ncu -i $O/$name.ncu-rep --page raw --csv > $O/raw_$name.csv
 ncu -i $O/$name.ncu-rep --page details > $O/details_$name.txt
 for k in 0 1; do
-ncu -i $O/$name.ncu-rep --launch-skip $k --launch-count 1 --page source --csv --print-source cuda --resolve-source-file $O/src/$srcf > $O/source_${name}_$k.csv 2>&1 || true
+ncu -i $O/$name.ncu-rep --launch-skip $k --launch-count 1 --page source --csv --print-source cuda,sass --resolve-source-file $O/src/$srcf > $O/source_${name}_$k.csv 2>&1 || true
 ncu -i $O/$name.ncu-rep --launch-skip $k --launch-count 1 --page source --csv --print-source sass > $O/sass_${name}_$k.csv 2>&1 || true
 done
 rm -f $O/$name.ncu-rep

@@ -63,6 +63,8 @@ struct KernelSpec {
   std::vector<std::vector<int>> soa_rows;
   std::vector<std::uint8_t> soa_arrays;  // tile modes: per array, 1 = elem_comp inputs read
                                          // from a tile-ordered SoA copy a.arr[i][c * soa_n + t]
+  int meta_depth_h = 1;       // tile reduction: segments' metadata loaded this many rounds ahead
+  int meta_depth_g = 1;       // (Hessian / gradient segments; registers across the barrier)
   bool plan_global = false;   // tile modes: read the plan slice from global memory (L2) instead of
                               // prefetching it to shared memory (keeps two CTAs per SM)
   int value_reduce = 0;    // value_only over items: 1 = max (activation), 2 = min/NaN->-inf (guard)

@@ -171,6 +171,7 @@ struct Energy {
   int* d_tile_perm = nullptr;  // tile position -> active ordinal (Morton order)
   int* d_tile_elems = nullptr; // tile position -> element id
   int cap[4] = {0, 0, 0, 0};   // shared plan-slice capacities (words): hseg, gseg, hcon, gcon
+  int meta_depth[2] = {1, 1};  // tile reduction: metadata prefetch depth (Hessian, gradient segments)
   double* d_gstage = nullptr;  // global staging (large elements): one slab per tile
   // tile-ordered SoA copies of wide per-element arrays (elem_comp inputs): array -> copy
   int* d_changed = nullptr;     // activation: "the active set moved" flag of the last refresh
@@ -658,6 +659,8 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.item_lanes = tile_item_lanes(e);
       s.soa_arrays = soa_arrays_of(c, e);
       s.soa_rows = soa_rows_spec(c, e);
+      s.meta_depth_h = e.meta_depth[0];
+      s.meta_depth_g = e.meta_depth[1];
       s.conn_soa = use_conn_soa();
       s.mode = OutMode::fused_tile;
       s.schedule = -1;  // auto: lowest peak of live values
@@ -673,6 +676,8 @@ KernelSpec spec_for(symel_cuda_ctx* c, Energy& e, Variant v) {
       s.plan_global = v == V_TILE_SPD_G;
       s.soa_arrays = soa_arrays_of(c, e);
       s.soa_rows = soa_rows_spec(c, e);
+      s.meta_depth_h = e.meta_depth[0];
+      s.meta_depth_g = e.meta_depth[1];
       // measured: the SPD tet kernel (compute-bound, its connectivity latency hidden behind the
       // other CTA's eigen-solve) is 1.3 % slower reading the copy; the exact-rounding contact
       // kernel (random nodes, latency-bound) gains
@@ -1042,6 +1047,26 @@ void ensure_tile_plan(symel_cuda_ctx* c) {
     // 32-bit words of the u16 slices, each copied as the 16-byte aligned range around it (bulk
     // copy) and starting 16-byte aligned in shared memory
     for (int q = 0; q < 4; ++q) e.cap[q] = ((2 * mx[q] + 30) / 16 + 1) * 4;
+    // Metadata prefetch depth of the tile reduction. A thread takes every T-th segment of its
+    // tile; with one or two contributions per segment (contact pairs: every block of a pair is its
+    // own segment, 10 rounds per thread) a round is much shorter than the metadata's load
+    // latency, so a one-deep prefetch exposes it every round (ncu: 21 % of the contact kernel's
+    // stall samples). Tiles with many short rounds prefetch four rounds ahead (config 5: depth
+    // 1 / 2 / 4 / 6 / 11 on the Hessian segments 14.22 / 14.06 / 13.90 / 14.05 / 14.09 ms with the
+    // gradient segments at 4; both at 1: 14.50); tiles with few, long rounds (tets: 3) keep
+    // depth 1 (deeper measured slower there: more live registers across the barrier).
+    {
+      const int T = tile_threads(c, e);
+      const int rounds_h = (mx[0] + T - 1) / T, rounds_g = (mx[1] + T - 1) / T;
+      int dh = rounds_h >= 6 ? 4 : 1, dg = rounds_g >= 3 ? 4 : 1;
+      if (const char* v = std::getenv("SYMEL_META_DEPTH_H")) dh = std::max(1, std::atoi(v));
+      if (const char* v = std::getenv("SYMEL_META_DEPTH_G")) dg = std::max(1, std::atoi(v));
+      if (dh != e.meta_depth[0] || dg != e.meta_depth[1]) {
+        e.meta_depth[0] = dh;
+        e.meta_depth[1] = dg;
+        for (int v : {V_TILE, V_TILE_SPD, V_TILE_G, V_TILE_SPD_G}) e.k[v] = nullptr;  // owned by the context's cache
+      }
+    }
     cfree(e.d_gstage);
     e.d_gstage = nullptr;
     if (nt > 0 && tile_global_stage(c, e)) dalloc(&e.d_gstage, (std::size_t)nt * tile_stage_doubles(c, e));

@@ -281,3 +281,34 @@ def test_non_finite_names_lowest_element_across_tiles(mode, oracle_mod):
             A.assemble(mode)
         m = re.search(r"element (\d+)", str(ei.value))
         assert m and int(m.group(1)) == ref["bad_element"], (str(ei.value), ref["bad_element"])
+
+
+@pytest.mark.parametrize("depth", [(2, 1), (4, 4), (12, 6)])
+@pytest.mark.parametrize("kind", ["contact", "tet10", "cloth"])
+def test_metadata_prefetch_depth(kind, depth, oracle_mod, monkeypatch):
+    """The tile reduction's segment-metadata prefetch depth (chosen from the plan: deeper for
+    tiles with many short rounds, symel_cuda.cpp Energy::meta_depth) only changes when loads are
+    issued: every depth gives the deterministic result of depth 1, bit for bit, and matches the
+    oracle. Depths beyond the number of rounds of a tile (predicated-off loads) included."""
+    case = {"contact": lambda: C.config5(3, 400), "tet10": lambda: C.config3(3), "cloth": lambda: C.config4(12)}[kind]()
+    spd = kind == "contact"
+    monkeypatch.setenv("SYMEL_META_DEPTH_H", "1")
+    monkeypatch.setenv("SYMEL_META_DEPTH_G", "1")
+    base = S.DeviceSystem(case, tapes=golden_tape, spd=spd)
+    E0 = base.asm.assemble("deterministic")
+    g0, H0 = base.asm.gradient(), base.asm.hessian().values
+    monkeypatch.setenv("SYMEL_META_DEPTH_H", str(depth[0]))
+    monkeypatch.setenv("SYMEL_META_DEPTH_G", str(depth[1]))
+    ds = S.DeviceSystem(case, tapes=golden_tape, spd=spd)
+    E = ds.asm.assemble("deterministic")
+    assert E == E0
+    assert np.array_equal(ds.asm.gradient().view(np.uint64), g0.view(np.uint64))
+    assert np.array_equal(ds.asm.hessian().values.view(np.uint64), H0.view(np.uint64))
+    if not spd:
+        ref = oracle_mod.system_for_case(case, golden_tape).assemble()
+        assert abs(E - ref["E"]) <= 1e-10 * max(1.0, abs(ref["E"]))
+        assert oracle_mod.rel_err(ds.asm.gradient(), ref["grad"]) <= 1e-10
+        assert oracle_mod.rel_err(ds.asm.hessian().values, ref["vals"]) <= 1e-10
+    Ea = ds.asm.assemble("atomic")
+    assert abs(Ea - E0) <= 1e-12 * max(1.0, abs(E0))
+    assert oracle_mod.rel_err(ds.asm.hessian().values, H0) <= 1e-12

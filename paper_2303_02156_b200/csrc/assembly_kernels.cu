@@ -449,12 +449,17 @@ int energy_serial(const double* const* elemE, const long long* strides, const lo
 int energy_tree(const double* v, long long stride, long long n, double* partial, double* out, void* s) {
   if (n == 0) return (int)cudaMemsetAsync(out, 0, sizeof(double), S(s));
   const long long nb = (n + kTreeChunk - 1) / kTreeChunk;
+  if (nb == 1) {  // one chunk: its tree sum is the result (the final pass would only add zeros to it)
+    k_tree_partial<<<1, kTreeThreads, 0, S(s)>>>(v, stride, n, out);
+    return (int)cudaGetLastError();
+  }
   k_tree_partial<<<(unsigned)nb, kTreeThreads, 0, S(s)>>>(v, stride, n, partial);
   k_tree_final<<<1, kTreeThreads, 0, S(s)>>>(partial, nb, out);
   return (int)cudaGetLastError();
 }
 
 long long energy_tree_partials(long long n) { return (n + kTreeChunk - 1) / kTreeChunk; }
+int energy_tree_launches(long long n) { return n <= 0 ? 0 : (n <= kTreeChunk ? 1 : 2); }
 
 int energy_combine(const double* per_energy, int n, double* out, void* s) {
   k_combine<<<1, 32, 0, S(s)>>>(per_energy, n, out);

@@ -75,6 +75,7 @@ int energy_serial(const double* const* elemE, const long long* strides, const lo
 // deterministic fixed-shape tree sum of n values (strided)
 int energy_tree(const double* v, long long stride, long long n, double* partial, double* out, void* stream);
 long long energy_tree_partials(long long n);
+int energy_tree_launches(long long n);  // kernels energy_tree enqueues for n values
 // combine per-energy totals in energy order (out = ((0 + e0) + e1) + ...)
 int energy_combine(const double* per_energy, int n, double* out, void* stream);
 

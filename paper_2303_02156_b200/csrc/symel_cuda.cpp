@@ -1247,7 +1247,7 @@ void enqueue_tiled(symel_cuda_ctx* c, const std::vector<TileLaunch>& ls, bool at
     if (e.skip || e.n_active == 0) continue;
     const long long nt = (e.n_active + tile_elems(c, e) - 1) / tile_elems(c, e);
     CK(dev::tile_energy(c->d_tileE, e.tile_base, nt, c->d_partial, c->d_energy + q, c->stream));
-    c->launches += 2;
+    c->launches += dev::energy_tree_launches(nt);
   }
   CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
   ++c->launches;
@@ -1429,7 +1429,7 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
       Energy& e = *c->energies[q];
       if (e.skip || e.n_active == 0) continue;
       CK(dev::energy_tree(e.d_contrib, e.deriv.n_outputs, e.n_active, c->d_partial, c->d_energy + q, c->stream));
-      c->launches += 2;
+      c->launches += dev::energy_tree_launches(e.n_active);
     }
   } else {
     for (int q = 0; q < ne; ++q) {
@@ -1439,7 +1439,7 @@ double do_assemble(symel_cuda_ctx* c, std::uint32_t flags, symel_cuda_status* st
       const double* v = staged ? e.d_contrib : e.d_elemE;
       const long long stride = staged ? e.deriv.n_outputs : 1;
       CK(dev::energy_tree(v, stride, e.n_active, c->d_partial, c->d_energy + q, c->stream));
-      c->launches += 2;
+      c->launches += dev::energy_tree_launches(e.n_active);
     }
     CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
     ++c->launches;
@@ -1872,7 +1872,7 @@ int symel_cuda_energy_only(symel_cuda_ctx* c, double* out) {
       a.value_out = e.d_elemE;
       launch(c, k, a, e.n_active);
       CK(dev::energy_tree(e.d_elemE, 1, e.n_active, c->d_partial, c->d_energy + q, c->stream));
-      c->launches += 2;
+      c->launches += dev::energy_tree_launches(e.n_active);
     }
     CK(dev::energy_combine(c->d_energy, ne, c->d_energy + ne, c->stream));
     CK(cudaMemcpyAsync(c->h_pinned, c->d_energy + ne, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
